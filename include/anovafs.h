@@ -1,0 +1,129 @@
+/*
+ * anovafs.h — C ABI of the B200-native ANOVA fast-summation matvec.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 2111.10140, package
+ * nfftkrr; paths relative to /root/reference/pkg/src/nfftkrr):
+ *
+ *   afs_plan_create   replaces the per-window construction in
+ *                     AnovaKernelOperator.__init__ (anova.py:146-173), i.e. one
+ *                     FastsumOperator per window (fastsum.py:189-232) with its
+ *                     NfftPlan geometry (nfft.py:139-177).  Scaling parameters
+ *                     (center/scale, fastsum.py:210-217) and the spectral
+ *                     multiplier (c_hat * deconv^2, fastsum.py:138-159 +
+ *                     nfft.py:158-162) are computed by the host layer and passed in.
+ *   afs_apply         replaces AnovaKernelOperator.apply (anova.py:175-183) =
+ *                     sum_l eta_l FastsumOperator.apply (fastsum.py:243-256) =
+ *                     Re(NfftPlan.forward(c_hat * NfftPlan.adjoint(alpha)))
+ *                     (nfft.py:220-250), for nrhs right-hand sides at once.
+ *   afs_cg_solve      replaces cg_solve(lambda v: op.apply(v) + beta*v, b, tol,
+ *                     maxiter) as called by fit (krr.py:76-110, 162-167), run
+ *                     device-resident with the same stopping rule and breakdown
+ *                     checks.
+ *   afs_last_error    message for the last non-zero status on this thread.
+ *
+ * Status codes map 1:1 onto the reference's exceptions (errors.py:8-17):
+ *   AFS_ERR_SHAPE -> ShapeError, AFS_ERR_VALIDATION -> ValidationError,
+ *   AFS_ERR_NUMERICAL -> NumericalError; AFS_ERR_CUDA / AFS_ERR_NOMEM are
+ *   device failures (RuntimeError / MemoryError on the Python side).
+ *
+ * Pointers: bulk arrays (coordinates, alpha, out, b, x) are DEVICE pointers on
+ * desc->device; small parameter arrays are HOST pointers.  All arithmetic is
+ * IEEE fp64.  A plan is immutable after creation; afs_apply / afs_cg_solve on
+ * one plan are serialised internally (the plan owns one workspace), so they
+ * are safe to call from several host threads.
+ */
+#ifndef ANOVAFS_H
+#define ANOVAFS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFS_ABI_VERSION 1
+
+enum afs_status {
+  AFS_OK = 0,
+  AFS_ERR_SHAPE = 1,
+  AFS_ERR_VALIDATION = 2,
+  AFS_ERR_NUMERICAL = 3,
+  AFS_ERR_CUDA = 4,
+  AFS_ERR_NOMEM = 5
+};
+
+typedef struct afs_plan afs_plan;
+
+/* One feature window W_l (anova.py:91-121; fastsum.py:189-232). */
+typedef struct afs_window_desc {
+  int32_t dims;              /* d_l in 1..3 */
+  int32_t features[3];       /* 0-based column indices into the coordinate matrix */
+  double center[3];          /* bbox centre of sources (U targets), fastsum.py:217 */
+  double scale;              /* ball_radius / bbox diameter, fastsum.py:216 */
+  double weight;             /* eta_l; the reference uses 1/P (anova.py:109) */
+  /* HOST pointer to the window's real, pruned spectral multiplier E (see
+   * DESIGN.md "spectral stage"): layout [j0][j1][k] for d=3, [j0][k] for d=2,
+   * [k] for d=1, with j in 0..M (frequency j - M/2) and k in 0..M/2, already
+   * symmetrised, scaled by 1/n^(2d) and doubled for k >= 1. */
+  const double* multiplier;
+} afs_window_desc;
+
+typedef struct afs_plan_desc {
+  int32_t device;            /* CUDA ordinal */
+  int32_t n_windows;         /* P >= 1 */
+  const afs_window_desc* windows;
+  int32_t d_total;           /* columns of the coordinate matrices */
+  int64_t n_sources;         /* N_x >= 1 */
+  const double* sources;     /* device, row-major n_sources x d_total */
+  int64_t n_targets;         /* 0 => targets are the sources */
+  const double* targets;     /* device, row-major n_targets x d_total, or NULL */
+  int32_t bandwidth;         /* M = PeriodizationConfig.coeff_grid (even >= 2) */
+  int32_t cutoff;            /* m = AccuracyProfile.cutoff (1..8) */
+  int32_t grid;              /* n = max(2m, even(ceil(oversampling*M))), nfft.py:151-153 */
+  int32_t max_rhs;           /* largest nrhs passed to afs_apply (>= 1) */
+} afs_plan_desc;
+
+typedef struct afs_plan_info {
+  int64_t device_bytes;      /* bytes of device memory owned by the plan */
+  int32_t n_windows;
+  int32_t grid;
+  int64_t n_sources;
+  int64_t n_targets;
+  int32_t kernel_launches_per_apply;
+} afs_plan_info;
+
+int afs_abi_version(void);
+const char* afs_last_error(void);
+
+int afs_plan_create(const afs_plan_desc* desc, afs_plan** plan);
+int afs_plan_destroy(afs_plan* plan);
+int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info);
+
+/* out[r*ld_out + i] = sum_l eta_l (K_l alpha_r)(z_i), r < nrhs.
+ * alpha: device, nrhs vectors of n_sources (stride ld_alpha);
+ * out:   device, nrhs vectors of n_targets (stride ld_out).
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out,
+              int64_t ld_out, int32_t nrhs, void* stream);
+
+/* Stage profiling: when enabled, every afs_apply records CUDA events around
+ * its spread / spectral / gather stages on the caller's stream, waits for them
+ * and accumulates the device milliseconds (this adds one stream sync per
+ * apply, so enable it only for a dedicated measurement pass).
+ * afs_plan_stage_times writes {spread_ms, spectral_ms, gather_ms, applies}
+ * and resets the accumulators when reset != 0. */
+int afs_plan_set_profiling(afs_plan* plan, int32_t enable);
+int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset);
+
+/* Solve (K + beta I) x = b by plain CG from x0 = 0 (krr.py:76-110).
+ * Requires n_targets == n_sources (no separate targets).  b, x: device.
+ * Returns AFS_ERR_NUMERICAL on breakdown with *iterations = failing iteration. */
+int afs_cg_solve(afs_plan* plan, const double* b, double* x, double beta, double tol,
+                 int32_t maxiter, int32_t* iterations, double* residual,
+                 int32_t* converged, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ANOVAFS_H */

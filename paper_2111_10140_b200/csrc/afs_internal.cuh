@@ -1,0 +1,135 @@
+// Internal definitions shared by the anovafs CUDA sources (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/anovafs.h"
+
+#define AFS_MAX_CUTOFF 8
+
+namespace afs {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct Error : public std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what);
+#define AFS_CUDA(call) ::afs::check_cuda((call), #call)
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct Window {
+  int d;
+  int feat[3];
+  double center[3];
+  double scale;
+  double eta;
+  int64_t cells;       // n^d
+  int64_t grid_off;    // offset of this window's grid block (per rhs: cells)
+  int64_t mult_len;    // (M+1)^(d-1) * (M/2+1)
+  int64_t mult_off;    // offset into plan->mult
+};
+
+struct CgScratch {
+  double* r = nullptr;
+  double* p = nullptr;
+  double* ap = nullptr;
+  double* partial = nullptr;   // reduction partials
+  double* scalars = nullptr;   // device scalars (see cg.cu)
+  double* host_scalars = nullptr;  // pinned
+  int64_t n = 0;
+};
+
+}  // namespace afs
+
+struct afs_plan {
+  int device = 0;
+  int P = 0;
+  int dtot = 0;
+  int64_t Ns = 0, Nt = 0;
+  bool has_targets = false;
+  int M = 0, m = 0, n = 0, H = 0;   // H = M/2 + 1
+  double b = 0.0;                   // Kaiser-Bessel shape pi(2 - M/n)
+  int max_rhs = 1;
+  std::vector<afs::Window> win;
+  afs::Window* d_win = nullptr;     // device copy of win
+  double* src = nullptr;            // device, row-major Ns x dtot
+  double* tgt = nullptr;            // device, row-major Nt x dtot (nullptr -> src)
+  double* mult = nullptr;           // all multipliers
+  double2* twiddle = nullptr;       // n entries e^{-2 pi i k / n}
+  double* grids = nullptr;          // [rhs][sum of cells]  (rhs-major)
+  int64_t grid_total = 0;           // sum of cells over windows
+  double2* scratch_a = nullptr;
+  double2* scratch_b = nullptr;
+  int64_t scratch_a_len = 0, scratch_b_len = 0;   // complex entries per rhs
+  afs::CgScratch cg;
+  int64_t device_bytes = 0;
+  int launches_per_apply = 0;
+  bool profiling = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double stage_ms[3] = {0.0, 0.0, 0.0};
+  int64_t profiled_applies = 0;
+  std::mutex mu;
+};
+
+namespace afs {
+
+// stages (implemented in spread.cu / spectral.cu / gather.cu / cg.cu)
+void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s);
+void spectral_all(afs_plan* p, int R, cudaStream_t s);
+void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
+void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                int R, cudaStream_t s);
+void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
+                   int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
+void make_twiddles(afs_plan* p);
+
+// ---------------------------------------------------------------------------
+// device helpers: exact mirror of the reference window arithmetic
+// ---------------------------------------------------------------------------
+// Kaiser-Bessel window, nfft.py:118-122.  Each product/difference is rounded
+// separately (no FMA contraction) to follow numpy's evaluation order.
+__device__ __forceinline__ double kb_window(double dist, int m, double b) {
+  const double mm = (double)(m * m);
+  const double arg = sqrt(fmax(__dsub_rn(mm, __dmul_rn(dist, dist)), 0.0));
+  if (arg > 1e-12) {
+    const double safe = fmax(arg, 1e-300);
+    return sinh(__dmul_rn(b, arg)) / __dmul_rn(3.141592653589793, safe);
+  }
+  return b / 3.141592653589793;
+}
+
+// Per-dimension stencil of one node (nfft.py:166-174): base cell u = floor(n x),
+// cells u+1-m .. u+m reduced mod n, weights phi(n x - cell).
+template <int MM>
+__device__ __forceinline__ void stencil_1d(double xs, int n, double b, double (&w)[2 * MM],
+                                           int (&idx)[2 * MM]) {
+  const double nx = __dmul_rn((double)n, xs);
+  const double u = floor(nx);
+  const long long ui = (long long)u;
+#pragma unroll
+  for (int o = 0; o < 2 * MM; ++o) {
+    const double cell = u + (double)(o + 1 - MM);
+    w[o] = kb_window(__dsub_rn(nx, cell), MM, b);
+    long long c = (ui + (o + 1 - MM)) % n;
+    idx[o] = (int)(c < 0 ? c + n : c);
+  }
+}
+
+// scaled coordinate (fastsum.py:229): (x - center) * scale
+__device__ __forceinline__ double scaled_coord(double x, double c, double s) {
+  return __dmul_rn(__dsub_rn(x, c), s);
+}
+
+}  // namespace afs

@@ -1,0 +1,282 @@
+// C ABI entry points (include/anovafs.h): plan construction, apply, CG.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "afs_internal.cuh"
+
+namespace afs {
+
+static thread_local std::string g_last_error;
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation)
+    throw Error(AFS_ERR_NOMEM, std::string("device allocation failed: ") + what);
+  throw Error(AFS_ERR_CUDA, std::string(cudaGetErrorString(e)) + " in " + what);
+}
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return AFS_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return AFS_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return AFS_ERR_CUDA;
+  }
+}
+
+void make_twiddles(afs_plan* p) {
+  std::vector<double2> tw(p->n);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < p->n; ++k) {
+    const long double a = two_pi * (long double)k / (long double)p->n;
+    tw[k] = make_double2((double)cosl(a), (double)-sinl(a));
+  }
+  AFS_CUDA(cudaMalloc(&p->twiddle, sizeof(double2) * p->n));
+  AFS_CUDA(cudaMemcpy(p->twiddle, tw.data(), sizeof(double2) * p->n, cudaMemcpyHostToDevice));
+  p->device_bytes += sizeof(double2) * p->n;
+}
+
+void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo, int R,
+                cudaStream_t s) {
+  if (!p->profiling) {
+    spread_all(p, alpha, lda, R, s);
+    spectral_all(p, R, s);
+    gather_all(p, out, ldo, R, s);
+    return;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (!p->ev[i]) AFS_CUDA(cudaEventCreate(&p->ev[i]));
+  AFS_CUDA(cudaEventRecord(p->ev[0], s));
+  spread_all(p, alpha, lda, R, s);
+  AFS_CUDA(cudaEventRecord(p->ev[1], s));
+  spectral_all(p, R, s);
+  AFS_CUDA(cudaEventRecord(p->ev[2], s));
+  gather_all(p, out, ldo, R, s);
+  AFS_CUDA(cudaEventRecord(p->ev[3], s));
+  AFS_CUDA(cudaEventSynchronize(p->ev[3]));
+  for (int i = 0; i < 3; ++i) {
+    float ms = 0.f;
+    AFS_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+    p->stage_ms[i] += ms;
+  }
+  p->profiled_applies += 1;
+}
+
+static void free_plan(afs_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaFree(p->d_win);
+  cudaFree(p->src);
+  cudaFree(p->tgt);
+  cudaFree(p->mult);
+  cudaFree(p->twiddle);
+  cudaFree(p->grids);
+  cudaFree(p->scratch_a);
+  cudaFree(p->scratch_b);
+  cudaFree(p->cg.r);
+  cudaFree(p->cg.p);
+  cudaFree(p->cg.ap);
+  cudaFree(p->cg.partial);
+  cudaFree(p->cg.scalars);
+  for (int i = 0; i < 4; ++i)
+    if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
+  delete p;
+}
+
+static void create_plan(const afs_plan_desc* d, afs_plan** out) {
+  if (!d || !out) throw Error(AFS_ERR_VALIDATION, "null descriptor or output pointer");
+  if (d->n_windows < 1 || !d->windows) throw Error(AFS_ERR_VALIDATION, "window set must not be empty");
+  if (d->d_total < 1) throw Error(AFS_ERR_SHAPE, "coordinate matrix must have >= 1 column");
+  if (d->n_sources < 1 || !d->sources)
+    throw Error(AFS_ERR_SHAPE, "sources must form a nonempty (N, d) matrix");
+  if (d->n_targets < 0 || (d->n_targets > 0 && !d->targets))
+    throw Error(AFS_ERR_SHAPE, "targets pointer missing");
+  if (d->bandwidth < 2 || d->bandwidth % 2)
+    throw Error(AFS_ERR_VALIDATION, "bandwidth M must be even and >= 2");
+  if (d->cutoff < 1 || d->cutoff > AFS_MAX_CUTOFF)
+    throw Error(AFS_ERR_VALIDATION, "window cutoff m must lie in 1..8");
+  if (d->grid % 2 || d->grid < 2 * d->cutoff || d->grid < d->bandwidth + 2 || d->grid > 2048)
+    throw Error(AFS_ERR_VALIDATION, "oversampled grid n must be even, >= max(2m, M+2), <= 2048");
+  if (d->max_rhs < 1) throw Error(AFS_ERR_VALIDATION, "max_rhs must be >= 1");
+
+  AFS_CUDA(cudaSetDevice(d->device));
+  afs_plan* p = new afs_plan();
+  try {
+    p->device = d->device;
+    p->P = d->n_windows;
+    p->dtot = d->d_total;
+    p->Ns = d->n_sources;
+    p->has_targets = d->n_targets > 0;
+    p->Nt = p->has_targets ? d->n_targets : d->n_sources;
+    p->M = d->bandwidth;
+    p->m = d->cutoff;
+    p->n = d->grid;
+    p->H = p->M / 2 + 1;
+    p->b = 3.141592653589793 * (2.0 - (double)p->M / (double)p->n);   // nfft.py:156
+    p->max_rhs = d->max_rhs;
+
+    const int K = p->M + 1;
+    int64_t grid_total = 0, mult_total = 0, a_len = 0, b_len = 0;
+    int launches = 2;   // memset + gather
+    p->win.resize(p->P);
+    for (int l = 0; l < p->P; ++l) {
+      const afs_window_desc& wd = d->windows[l];
+      Window& w = p->win[l];
+      if (wd.dims < 1 || wd.dims > 3)
+        throw Error(AFS_ERR_VALIDATION, "window size must be 1..3");
+      if (!wd.multiplier) throw Error(AFS_ERR_VALIDATION, "window multiplier missing");
+      if (!(wd.scale > 0.0) || !std::isfinite(wd.scale))
+        throw Error(AFS_ERR_VALIDATION, "window scale must be positive and finite");
+      w.d = wd.dims;
+      for (int t = 0; t < 3; ++t) {
+        w.feat[t] = t < wd.dims ? wd.features[t] : 0;
+        w.center[t] = t < wd.dims ? wd.center[t] : 0.0;
+        if (t < wd.dims && (wd.features[t] < 0 || wd.features[t] >= p->dtot))
+          throw Error(AFS_ERR_VALIDATION, "window feature index out of range");
+      }
+      w.scale = wd.scale;
+      w.eta = wd.weight;
+      w.cells = 1;
+      for (int t = 0; t < w.d; ++t) w.cells *= p->n;
+      w.grid_off = grid_total;
+      grid_total += w.cells;
+      w.mult_len = p->H;
+      for (int t = 1; t < w.d; ++t) w.mult_len *= K;
+      w.mult_off = mult_total;
+      mult_total += w.mult_len;
+      if (w.d == 2) a_len = std::max<int64_t>(a_len, (int64_t)p->n * p->H);
+      if (w.d == 3) {
+        a_len = std::max<int64_t>(a_len, (int64_t)p->n * p->n * p->H);
+        b_len = std::max<int64_t>(b_len, (int64_t)p->n * K * p->H);
+      }
+      launches += 1 + (w.d == 1 ? 1 : (w.d == 2 ? 3 : 5));
+    }
+    p->grid_total = grid_total;
+    p->launches_per_apply = launches;
+
+    const size_t src_bytes = sizeof(double) * p->Ns * p->dtot;
+    AFS_CUDA(cudaMalloc(&p->src, src_bytes));
+    AFS_CUDA(cudaMemcpy(p->src, d->sources, src_bytes, cudaMemcpyDeviceToDevice));
+    p->device_bytes += src_bytes;
+    if (p->has_targets) {
+      const size_t tb = sizeof(double) * p->Nt * p->dtot;
+      AFS_CUDA(cudaMalloc(&p->tgt, tb));
+      AFS_CUDA(cudaMemcpy(p->tgt, d->targets, tb, cudaMemcpyDeviceToDevice));
+      p->device_bytes += tb;
+    }
+    std::vector<double> mult(mult_total);
+    for (int l = 0; l < p->P; ++l)
+      std::memcpy(mult.data() + p->win[l].mult_off, d->windows[l].multiplier,
+                  sizeof(double) * p->win[l].mult_len);
+    AFS_CUDA(cudaMalloc(&p->mult, sizeof(double) * mult_total));
+    AFS_CUDA(cudaMemcpy(p->mult, mult.data(), sizeof(double) * mult_total, cudaMemcpyHostToDevice));
+    AFS_CUDA(cudaMalloc(&p->d_win, sizeof(Window) * p->P));
+    AFS_CUDA(cudaMemcpy(p->d_win, p->win.data(), sizeof(Window) * p->P, cudaMemcpyHostToDevice));
+    AFS_CUDA(cudaMalloc(&p->grids, sizeof(double) * grid_total * p->max_rhs));
+    p->device_bytes += sizeof(double) * (mult_total + grid_total * p->max_rhs) + sizeof(Window) * p->P;
+    p->scratch_a_len = a_len;
+    p->scratch_b_len = b_len;
+    if (a_len) AFS_CUDA(cudaMalloc(&p->scratch_a, sizeof(double2) * a_len * p->max_rhs));
+    if (b_len) AFS_CUDA(cudaMalloc(&p->scratch_b, sizeof(double2) * b_len * p->max_rhs));
+    p->device_bytes += sizeof(double2) * (a_len + b_len) * p->max_rhs;
+    make_twiddles(p);
+    AFS_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    free_plan(p);
+    throw;
+  }
+  *out = p;
+}
+
+}  // namespace afs
+
+extern "C" {
+
+int afs_abi_version(void) { return AFS_ABI_VERSION; }
+
+const char* afs_last_error(void) { return afs::g_last_error.c_str(); }
+
+int afs_plan_create(const afs_plan_desc* desc, afs_plan** plan) {
+  return afs::guarded([&] { afs::create_plan(desc, plan); });
+}
+
+int afs_plan_destroy(afs_plan* plan) {
+  return afs::guarded([&] { afs::free_plan(plan); });
+}
+
+int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info) {
+  return afs::guarded([&] {
+    if (!plan || !info) throw afs::Error(AFS_ERR_VALIDATION, "null plan or info");
+    info->device_bytes = plan->device_bytes;
+    info->n_windows = plan->P;
+    info->grid = plan->n;
+    info->n_sources = plan->Ns;
+    info->n_targets = plan->Nt;
+    info->kernel_launches_per_apply = plan->launches_per_apply;
+  });
+}
+
+int afs_plan_set_profiling(afs_plan* plan, int32_t enable) {
+  return afs::guarded([&] {
+    if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->profiling = enable != 0;
+  });
+}
+
+int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset) {
+  return afs::guarded([&] {
+    if (!plan || !out4) throw afs::Error(AFS_ERR_VALIDATION, "null plan/out");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    for (int i = 0; i < 3; ++i) out4[i] = plan->stage_ms[i];
+    out4[3] = (double)plan->profiled_applies;
+    if (reset) {
+      for (int i = 0; i < 3; ++i) plan->stage_ms[i] = 0.0;
+      plan->profiled_applies = 0;
+    }
+  });
+}
+
+int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out, int64_t ld_out,
+              int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
+    if (nrhs < 1 || nrhs > plan->max_rhs)
+      throw afs::Error(AFS_ERR_SHAPE, "nrhs must lie in 1..max_rhs");
+    if (!alpha || !out) throw afs::Error(AFS_ERR_SHAPE, "null alpha/out");
+    if (ld_alpha < plan->Ns || ld_out < plan->Nt)
+      throw afs::Error(AFS_ERR_SHAPE, "leading dimension smaller than vector length");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    afs::apply_impl(plan, alpha, ld_alpha, out, ld_out, nrhs, (cudaStream_t)stream);
+  });
+}
+
+int afs_cg_solve(afs_plan* plan, const double* b, double* x, double beta, double tol,
+                 int32_t maxiter, int32_t* iterations, double* residual, int32_t* converged,
+                 void* stream) {
+  int it = 0, conv = 0;
+  double res = 0.0;
+  const int st = afs::guarded([&] {
+    if (!plan || !b || !x) throw afs::Error(AFS_ERR_VALIDATION, "null plan/b/x");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    afs::cg_solve_impl(plan, b, x, beta, tol, maxiter, &it, &res, &conv, (cudaStream_t)stream);
+  });
+  if (iterations) *iterations = it;
+  if (residual) *residual = res;
+  if (converged) *converged = conv;
+  return st;
+}
+
+}  // extern "C"

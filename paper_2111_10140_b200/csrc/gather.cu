@@ -1,0 +1,108 @@
+// NFFT interpolation (nfft.py:228-229) for every window, accumulated across
+// windows in the reference's fixed order (anova.py:179-183):
+//     out_i <- out_i + eta_l * sum_stencil g_l[cell] * w(cell)
+//
+// v1 kernel: one thread per target node, all windows and all right-hand sides
+// in one launch; the stencil weights are computed once per (node, window) and
+// reused across right-hand sides.  Deterministic (no atomics).
+#include "afs_internal.cuh"
+
+namespace afs {
+
+template <int D, int MM>
+__device__ __forceinline__ void window_interp(const double* __restrict__ zrow, const Window& w,
+                                              int n, double b, const double* __restrict__ grids,
+                                              int64_t rhs_stride, int R, double* acc) {
+  double wt[D][2 * MM];
+  int ix[D][2 * MM];
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const double xs = scaled_coord(zrow[w.feat[t]], w.center[t], w.scale);
+    stencil_1d<MM>(xs, n, b, wt[t], ix[t]);
+  }
+  for (int r = 0; r < R; ++r) {
+    const double* g = grids + r * rhs_stride + w.grid_off;
+    double s = 0.0;
+    if (D == 1) {
+#pragma unroll
+      for (int o0 = 0; o0 < 2 * MM; ++o0) s += g[ix[0][o0]] * wt[0][o0];
+    } else if (D == 2) {
+#pragma unroll 1
+      for (int o0 = 0; o0 < 2 * MM; ++o0) {
+        const double* row = g + (int64_t)ix[0][o0] * n;
+#pragma unroll
+        for (int o1 = 0; o1 < 2 * MM; ++o1)
+          s += row[ix[D - 1][o1]] * __dmul_rn(wt[0][o0], wt[D - 1][o1]);
+      }
+    } else {
+#pragma unroll 1
+      for (int o0 = 0; o0 < 2 * MM; ++o0) {
+        const int64_t p0 = (int64_t)ix[0][o0] * n;
+#pragma unroll 1
+        for (int o1 = 0; o1 < 2 * MM; ++o1) {
+          const double* line = g + (p0 + ix[1 % D][o1]) * n;
+          const double w01 = __dmul_rn(wt[0][o0], wt[1 % D][o1]);
+#pragma unroll
+          for (int o2 = 0; o2 < 2 * MM; ++o2)
+            s += line[ix[D - 1][o2]] * __dmul_rn(w01, wt[D - 1][o2]);
+        }
+      }
+    }
+    acc[r] = __dadd_rn(acc[r], __dmul_rn(w.eta, s));
+  }
+}
+
+#define AFS_GATHER_RCHUNK 8
+
+template <int MM>
+__global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict__ Z, int64_t N,
+                                                       int dtot, const Window* __restrict__ wins,
+                                                       int P, int n, double b,
+                                                       const double* __restrict__ grids,
+                                                       int64_t rhs_stride, int R,
+                                                       double* __restrict__ out, int64_t ldo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const double* zrow = Z + i * dtot;
+  for (int r0 = 0; r0 < R; r0 += AFS_GATHER_RCHUNK) {
+    const int rc = min(AFS_GATHER_RCHUNK, R - r0);
+    double acc[AFS_GATHER_RCHUNK];
+#pragma unroll
+    for (int r = 0; r < AFS_GATHER_RCHUNK; ++r) acc[r] = 0.0;
+    const double* gr = grids + r0 * rhs_stride;
+    for (int l = 0; l < P; ++l) {
+      const Window w = wins[l];
+      if (w.d == 1)
+        window_interp<1, MM>(zrow, w, n, b, gr, rhs_stride, rc, acc);
+      else if (w.d == 2)
+        window_interp<2, MM>(zrow, w, n, b, gr, rhs_stride, rc, acc);
+      else
+        window_interp<3, MM>(zrow, w, n, b, gr, rhs_stride, rc, acc);
+    }
+    for (int r = 0; r < rc; ++r) out[(r0 + r) * ldo + i] = acc[r];
+  }
+}
+
+void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
+  const double* Z = p->has_targets ? p->tgt : p->src;
+  const int64_t N = p->Nt;
+  const int threads = 128;
+  const int64_t blocks = (N + threads - 1) / threads;
+#define AFS_G(MM)                                                                            \
+  k_gather_simple<MM><<<blocks, threads, 0, s>>>(Z, N, p->dtot, p->d_win, p->P, p->n, p->b, \
+                                                 p->grids, p->grid_total, R, out, ldo)
+  switch (p->m) {
+    case 1: AFS_G(1); break;
+    case 2: AFS_G(2); break;
+    case 3: AFS_G(3); break;
+    case 4: AFS_G(4); break;
+    case 5: AFS_G(5); break;
+    case 6: AFS_G(6); break;
+    case 7: AFS_G(7); break;
+    default: AFS_G(8); break;
+  }
+#undef AFS_G
+  AFS_CUDA(cudaGetLastError());
+}
+
+}  // namespace afs

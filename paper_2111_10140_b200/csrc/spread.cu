@@ -1,0 +1,96 @@
+// Adjoint-NFFT spreading (the bincount loop of nfft.py:232-245), all windows.
+//
+// v1 kernel: one thread per (node, window); the (2m)^d tensor-product stencil
+// is accumulated into the window's L2-resident real grid with native fp64
+// global reductions (RED.E.ADD.F64).  alpha is real, so the reference's
+// complex grid has zero imaginary part and only the real grid is kept.
+#include "afs_internal.cuh"
+
+namespace afs {
+
+template <int D, int MM>
+__global__ void __launch_bounds__(256) k_spread_red(const double* __restrict__ X, int64_t N,
+                                                    int dtot, Window w, int n, double b,
+                                                    const double* __restrict__ alpha,
+                                                    int64_t lda, int R, double* __restrict__ grid,
+                                                    int64_t rhs_stride) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double wt[D][2 * MM];
+  int ix[D][2 * MM];
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const double xs = scaled_coord(X[j * dtot + w.feat[t]], w.center[t], w.scale);
+    stencil_1d<MM>(xs, n, b, wt[t], ix[t]);
+  }
+  for (int r = 0; r < R; ++r) {
+    const double a = alpha[r * lda + j];
+    double* g = grid + r * rhs_stride + w.grid_off;
+    if (D == 1) {
+#pragma unroll
+      for (int o0 = 0; o0 < 2 * MM; ++o0) atomicAdd(g + ix[0][o0], __dmul_rn(a, wt[0][o0]));
+    } else if (D == 2) {
+#pragma unroll 1
+      for (int o0 = 0; o0 < 2 * MM; ++o0) {
+        const int64_t row = (int64_t)ix[0][o0] * n;
+#pragma unroll
+        for (int o1 = 0; o1 < 2 * MM; ++o1)
+          atomicAdd(g + row + ix[D - 1][o1], __dmul_rn(a, __dmul_rn(wt[0][o0], wt[D - 1][o1])));
+      }
+    } else {
+#pragma unroll 1
+      for (int o0 = 0; o0 < 2 * MM; ++o0) {
+        const int64_t p0 = (int64_t)ix[0][o0] * n;
+#pragma unroll 1
+        for (int o1 = 0; o1 < 2 * MM; ++o1) {
+          const int64_t p1 = (p0 + ix[1 % D][o1]) * n;
+          const double w01 = __dmul_rn(wt[0][o0], wt[1 % D][o1]);
+#pragma unroll
+          for (int o2 = 0; o2 < 2 * MM; ++o2)
+            atomicAdd(g + p1 + ix[D - 1][o2], __dmul_rn(a, __dmul_rn(w01, wt[D - 1][o2])));
+        }
+      }
+    }
+  }
+}
+
+template <int MM>
+static void launch_spread_m(afs_plan* p, const Window& w, const double* alpha, int64_t lda, int R,
+                            cudaStream_t s) {
+  const int threads = 256;
+  const int64_t blocks = (p->Ns + threads - 1) / threads;
+  const int64_t rs = p->grid_total;
+  switch (w.d) {
+    case 1:
+      k_spread_red<1, MM><<<blocks, threads, 0, s>>>(p->src, p->Ns, p->dtot, w, p->n, p->b, alpha,
+                                                     lda, R, p->grids, rs);
+      break;
+    case 2:
+      k_spread_red<2, MM><<<blocks, threads, 0, s>>>(p->src, p->Ns, p->dtot, w, p->n, p->b, alpha,
+                                                     lda, R, p->grids, rs);
+      break;
+    default:
+      k_spread_red<3, MM><<<blocks, threads, 0, s>>>(p->src, p->Ns, p->dtot, w, p->n, p->b, alpha,
+                                                     lda, R, p->grids, rs);
+      break;
+  }
+}
+
+void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
+  AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * p->grid_total * R, s));
+  for (const Window& w : p->win) {
+    switch (p->m) {
+      case 1: launch_spread_m<1>(p, w, alpha, lda, R, s); break;
+      case 2: launch_spread_m<2>(p, w, alpha, lda, R, s); break;
+      case 3: launch_spread_m<3>(p, w, alpha, lda, R, s); break;
+      case 4: launch_spread_m<4>(p, w, alpha, lda, R, s); break;
+      case 5: launch_spread_m<5>(p, w, alpha, lda, R, s); break;
+      case 6: launch_spread_m<6>(p, w, alpha, lda, R, s); break;
+      case 7: launch_spread_m<7>(p, w, alpha, lda, R, s); break;
+      default: launch_spread_m<8>(p, w, alpha, lda, R, s); break;
+    }
+  }
+  AFS_CUDA(cudaGetLastError());
+}
+
+}  // namespace afs
