@@ -45,6 +45,7 @@ class PlanDesc(ctypes.Structure):
         ("cutoff", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("max_rhs", ctypes.c_int32),
+        ("window_eval", ctypes.c_int32),
     ]
 
 

@@ -41,6 +41,9 @@ struct Window {
   int64_t mult_off;    // offset into plan->mult
 };
 
+struct SortedSide;   // geometry.cuh
+struct PolyTable;    // geometry.cuh
+
 struct CgScratch {
   double* r = nullptr;
   double* p = nullptr;
@@ -76,6 +79,10 @@ struct afs_plan {
   afs::CgScratch cg;
   int64_t device_bytes = 0;
   int launches_per_apply = 0;
+  // v2 geometry (window_eval == 0): per window, bin-sorted source / target nodes
+  int window_eval = 0;                 // 0 polynomial window + sliding kernels, 1 exact mirror (v1)
+  std::vector<afs::SortedSide*> src_side, tgt_side;
+  afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};

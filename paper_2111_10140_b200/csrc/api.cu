@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "afs_internal.cuh"
+#include "geometry.cuh"
 
 namespace afs {
 
@@ -90,6 +91,11 @@ static void free_plan(afs_plan* p) {
   for (int i = 0; i < 4; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
+  for (SortedSide* s : p->src_side)
+    if (s) { free_sorted_side(s); delete s; }
+  for (SortedSide* s : p->tgt_side)
+    if (s) { free_sorted_side(s); delete s; }
+  delete p->poly;
   delete p;
 }
 
@@ -190,6 +196,26 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
     if (b_len) AFS_CUDA(cudaMalloc(&p->scratch_b, sizeof(double2) * b_len * p->max_rhs));
     p->device_bytes += sizeof(double2) * (a_len + b_len) * p->max_rhs;
     make_twiddles(p);
+    if (d->window_eval != 0 && d->window_eval != 1)
+      throw Error(AFS_ERR_VALIDATION, "window_eval must be 0 (polynomial) or 1 (exact)");
+    p->window_eval = d->window_eval;
+    if (p->window_eval == 0) {
+      p->poly = new PolyTable();
+      make_poly_table(p->m, p->b, p->poly);
+      p->src_side.assign(p->P, nullptr);
+      p->tgt_side.assign(p->P, nullptr);
+      for (int l = 0; l < p->P; ++l) {
+        p->src_side[l] = new SortedSide();
+        build_sorted_side(p, p->win[l], p->src, p->Ns, p->src_side[l]);
+        if (p->has_targets) {
+          p->tgt_side[l] = new SortedSide();
+          build_sorted_side(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l]);
+        }
+      }
+      int launches = 0;
+      for (const Window& w : p->win) launches += 2 + (w.d == 1 ? 1 : (w.d == 2 ? 3 : 5));
+      p->launches_per_apply = launches;
+    }
     AFS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
     free_plan(p);

@@ -5,7 +5,10 @@
 // v1 kernel: one thread per target node, all windows and all right-hand sides
 // in one launch; the stencil weights are computed once per (node, window) and
 // reused across right-hand sides.  Deterministic (no atomics).
+#include <algorithm>
+
 #include "afs_internal.cuh"
+#include "sliding.cuh"
 
 namespace afs {
 
@@ -57,7 +60,7 @@ __device__ __forceinline__ void window_interp(const double* __restrict__ zrow, c
 template <int MM>
 __global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict__ Z, int64_t N,
                                                        int dtot, const Window* __restrict__ wins,
-                                                       int P, int n, double b,
+                                                       int l0, int l1, int n, double b,
                                                        const double* __restrict__ grids,
                                                        int64_t rhs_stride, int R,
                                                        double* __restrict__ out, int64_t ldo) {
@@ -68,9 +71,9 @@ __global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict_
     const int rc = min(AFS_GATHER_RCHUNK, R - r0);
     double acc[AFS_GATHER_RCHUNK];
 #pragma unroll
-    for (int r = 0; r < AFS_GATHER_RCHUNK; ++r) acc[r] = 0.0;
+    for (int r = 0; r < AFS_GATHER_RCHUNK; ++r) acc[r] = r < rc ? out[(r0 + r) * ldo + i] : 0.0;
     const double* gr = grids + r0 * rhs_stride;
-    for (int l = 0; l < P; ++l) {
+    for (int l = l0; l < l1; ++l) {
       const Window w = wins[l];
       if (w.d == 1)
         window_interp<1, MM>(zrow, w, n, b, gr, rhs_stride, rc, acc);
@@ -83,13 +86,14 @@ __global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict_
   }
 }
 
-void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
+// v1 interpolation of windows [l0, l1) added onto out (exact-mirror path / fallback)
+static void gather_v1(afs_plan* p, int l0, int l1, double* out, int64_t ldo, int R, cudaStream_t s) {
   const double* Z = p->has_targets ? p->tgt : p->src;
   const int64_t N = p->Nt;
   const int threads = 128;
   const int64_t blocks = (N + threads - 1) / threads;
-#define AFS_G(MM)                                                                            \
-  k_gather_simple<MM><<<blocks, threads, 0, s>>>(Z, N, p->dtot, p->d_win, p->P, p->n, p->b, \
+#define AFS_G(MM)                                                                              \
+  k_gather_simple<MM><<<blocks, threads, 0, s>>>(Z, N, p->dtot, p->d_win, l0, l1, p->n, p->b, \
                                                  p->grids, p->grid_total, R, out, ldo)
   switch (p->m) {
     case 1: AFS_G(1); break;
@@ -102,6 +106,41 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
     default: AFS_G(8); break;
   }
 #undef AFS_G
+}
+
+static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R, cudaStream_t s) {
+  if (p->window_eval != 0) return false;
+  const Window& w = p->win[l];
+  const SortedSide& sv = p->has_targets ? *p->tgt_side[l] : *p->src_side[l];
+  const int rg = v2_rhs_group(w.d, p->m, R);
+  if (rg < 1) return false;
+  for (int r0 = 0; r0 < R; r0 += rg) {
+    const int nr = std::min(rg, R - r0);
+    const double* g = p->grids + r0 * p->grid_total;
+    double* o = out + r0 * ldo;
+    bool ok = false;
+    switch (w.d) {
+      case 1: ok = launch_gather_v2<1>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+      case 2: ok = launch_gather_v2<2>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+      default: ok = launch_gather_v2<3>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+    }
+    if (!ok) {
+      if (r0 != 0) throw Error(AFS_ERR_CUDA, "inconsistent v2 gather dispatch");
+      return false;
+    }
+  }
+  return true;
+}
+
+void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
+  // out = 0, then out += eta_l * s_l in window order (anova.py:179-183)
+  AFS_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * p->Nt, R, s));
+  if (p->window_eval != 0) {
+    gather_v1(p, 0, p->P, out, ldo, R, s);
+  } else {
+    for (int l = 0; l < p->P; ++l)
+      if (!gather_v2_window(p, l, out, ldo, R, s)) gather_v1(p, l, l + 1, out, ldo, R, s);
+  }
   AFS_CUDA(cudaGetLastError());
 }
 

@@ -1,0 +1,169 @@
+// Plan-time geometry: per-window scaled node coordinates n*x (nfft.py:170-172
+// with fastsum.py:229 scaling), bin-sorted by base cell with a device radix
+// sort, and cut into column runs ("chunks") for the sliding-window kernels.
+#include <cmath>
+#include <cub/cub.cuh>
+
+#include "geometry.cuh"
+
+namespace afs {
+
+__global__ void k_prep_nodes(const double* __restrict__ X, int64_t N, int dtot, Window w, int n,
+                             double* __restrict__ nx_out, uint64_t* __restrict__ key,
+                             int32_t* __restrict__ idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  uint64_t k = 0;
+  for (int t = 0; t < w.d; ++t) {
+    const double xs = scaled_coord(X[j * dtot + w.feat[t]], w.center[t], w.scale);
+    const double nx = __dmul_rn((double)n, xs);             // nfft.py:170
+    nx_out[t * N + j] = nx;
+    long long u = (long long)floor(nx) % n;
+    if (u < 0) u += n;
+    k = k * (uint64_t)n + (uint64_t)u;
+  }
+  key[j] = k;
+  idx[j] = (int32_t)j;
+}
+
+__global__ void k_permute_nodes(const double* __restrict__ nx_in, const int32_t* __restrict__ idx,
+                                int64_t N, int d, double* __restrict__ nx_out,
+                                int32_t* __restrict__ perm) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t j = idx[i];
+  perm[i] = j;
+  for (int t = 0; t < d; ++t) nx_out[t * N + i] = nx_in[t * N + j];
+}
+
+__global__ void k_column_counts(const uint64_t* __restrict__ key, int64_t N, uint64_t n,
+                                int32_t* __restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  atomicAdd(&counts[key[i] / n], 1);
+}
+
+static int chunk_cap_for(int d) {
+  // one team of TEAM lanes per chunk; ~32 nodes per lane of work per chunk
+  return d == 3 ? 1024 : (d == 2 ? 256 : 32);
+}
+
+void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
+  if (N >= (int64_t)INT32_MAX) throw Error(AFS_ERR_VALIDATION, "at most 2^31-1 nodes per plan");
+  const int d = w.d, n = p->n;
+  const cudaStream_t s = 0;
+  int bits = 0;
+  {
+    long double cells = 1;
+    for (int t = 0; t < d; ++t) cells *= n;
+    while ((long double)(1ULL << bits) < cells && bits < 63) ++bits;
+  }
+  double* nx_tmp = nullptr;
+  uint64_t *key_a = nullptr, *key_b = nullptr;
+  int32_t *idx_a = nullptr, *idx_b = nullptr, *counts = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  auto cleanup = [&] {
+    cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
+    cudaFree(counts); cudaFree(temp);
+  };
+  try {
+    AFS_CUDA(cudaMalloc(&nx_tmp, sizeof(double) * d * N));
+    AFS_CUDA(cudaMalloc(&key_a, sizeof(uint64_t) * N));
+    AFS_CUDA(cudaMalloc(&key_b, sizeof(uint64_t) * N));
+    AFS_CUDA(cudaMalloc(&idx_a, sizeof(int32_t) * N));
+    AFS_CUDA(cudaMalloc(&idx_b, sizeof(int32_t) * N));
+    const int th = 256;
+    const int64_t bl = (N + th - 1) / th;
+    k_prep_nodes<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, nx_tmp, key_a, idx_a);
+    AFS_CUDA(cudaGetLastError());
+    AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key_a, key_b, idx_a, idx_b,
+                                             (int)N, 0, bits > 0 ? bits : 1, s));
+    AFS_CUDA(cudaMalloc(&temp, temp_bytes));
+    AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_a, key_b, idx_a, idx_b,
+                                             (int)N, 0, bits > 0 ? bits : 1, s));
+    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * d * N));
+    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * N));
+    k_permute_nodes<<<bl, th, 0, s>>>(nx_tmp, idx_b, N, d, out->nx, out->perm);
+    AFS_CUDA(cudaGetLastError());
+    // column runs
+    const int64_t ncol = d == 1 ? 1 : (d == 2 ? (int64_t)n : (int64_t)n * n);
+    AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * ncol));
+    AFS_CUDA(cudaMemset(counts, 0, sizeof(int32_t) * ncol));
+    k_column_counts<<<bl, th, 0, s>>>(key_b, N, (uint64_t)n, counts);
+    AFS_CUDA(cudaGetLastError());
+    std::vector<int32_t> hc(ncol);
+    AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * ncol, cudaMemcpyDeviceToHost));
+    const int cap = chunk_cap_for(d);
+    std::vector<Chunk> ch;
+    int64_t pos = 0;
+    for (int64_t c = 0; c < ncol; ++c) {
+      for (int32_t o = 0; o < hc[c]; o += cap)
+        ch.push_back(Chunk{(int32_t)c, std::min(cap, hc[c] - o), pos + o});
+      pos += hc[c];
+    }
+    out->N = N;
+    out->nchunks = (int64_t)ch.size();
+    out->chunk_cap = cap;
+    AFS_CUDA(cudaMalloc(&out->chunks, sizeof(Chunk) * std::max<size_t>(1, ch.size())));
+    AFS_CUDA(cudaMemcpy(out->chunks, ch.data(), sizeof(Chunk) * ch.size(), cudaMemcpyHostToDevice));
+    p->device_bytes += (int64_t)(sizeof(double) * d + sizeof(int32_t)) * N +
+                       (int64_t)sizeof(Chunk) * out->nchunks;
+    AFS_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+void free_sorted_side(SortedSide* s) {
+  cudaFree(s->nx);
+  cudaFree(s->perm);
+  cudaFree(s->chunks);
+  *s = SortedSide{};
+}
+
+// Chebyshev interpolation of phi(f + m - 1 - i) on f in [0, 1/2] at kPolyTerms nodes,
+// in extended precision, converted to monomials in x = f - 1/4 (u = 4x in [-1, 1]).
+void make_poly_table(int m, double b_d, PolyTable* tab) {
+  std::memset(tab, 0, sizeof(*tab));
+  const int N = kPolyTerms;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  const long double b = (long double)b_d;
+  for (int i = 0; i < 2 * m; ++i) {
+    long double vals[kPolyTerms], cheb[kPolyTerms];
+    for (int j = 0; j < N; ++j) {
+      const long double u = cosl(PI * (j + 0.5L) / N);
+      const long double f = (u + 1.0L) / 4.0L;
+      const long double t = f + (long double)(m - 1 - i);
+      const long double z = (long double)m * m - t * t;
+      const long double sq = z > 0 ? sqrtl(z) : 0.0L;
+      vals[j] = sq > 0 ? sinhl(b * sq) / (PI * sq) : b / PI;
+    }
+    for (int k = 0; k < N; ++k) {
+      long double acc = 0;
+      for (int j = 0; j < N; ++j) acc += vals[j] * cosl(PI * k * (j + 0.5L) / N);
+      cheb[k] = 2.0L * acc / N;
+    }
+    cheb[0] *= 0.5L;
+    // T_k(4x) as monomials in x
+    long double Tm1[kPolyTerms] = {0}, T0[kPolyTerms] = {0}, poly[kPolyTerms] = {0};
+    Tm1[0] = 1.0L;           // T_0
+    T0[1] = 4.0L;            // T_1 = 4x
+    for (int q = 0; q < N; ++q) poly[q] += cheb[0] * Tm1[q];
+    if (N > 1)
+      for (int q = 0; q < N; ++q) poly[q] += cheb[1] * T0[q];
+    for (int k = 2; k < N; ++k) {
+      long double Tn[kPolyTerms] = {0};
+      for (int q = 0; q + 1 < N; ++q) Tn[q + 1] += 8.0L * T0[q];
+      for (int q = 0; q < N; ++q) Tn[q] -= Tm1[q];
+      for (int q = 0; q < N; ++q) poly[q] += cheb[k] * Tn[q];
+      std::memcpy(Tm1, T0, sizeof(T0));
+      std::memcpy(T0, Tn, sizeof(Tn));
+    }
+    for (int q = 0; q < N; ++q) tab->c[i][q] = (double)poly[q];
+  }
+}
+
+}  // namespace afs

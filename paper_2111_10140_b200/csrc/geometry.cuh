@@ -1,0 +1,74 @@
+// Plan-time node geometry, bin-sorted per window (replaces NfftPlan's per-node
+// _idx/_w tables, nfft.py:164-174), and the device helpers the v2
+// spread/gather kernels share.
+#pragma once
+
+#include "afs_internal.cuh"
+
+namespace afs {
+
+constexpr int kPolyMaxOffsets = 2 * AFS_MAX_CUTOFF;   // 2m
+constexpr int kPolyTerms = 14;                        // degree 13 in x = f - 1/4
+
+// Kaiser-Bessel window as polynomials P_i(f) ~ phi(f + m - 1 - i), f in [0, 1/2],
+// monomial coefficients in x = f - 1/4 (index 0 = constant term).  Values for
+// f in (1/2, 1) follow from phi(f+m-1-i) = P_{2m-1-i}(1-f).
+struct PolyTable {
+  double c[kPolyMaxOffsets][kPolyTerms];
+};
+
+// A run of consecutive sorted nodes sharing one column (all but the last
+// dimension's base cell); processed by one team with one sliding window.
+struct Chunk {
+  int32_t col;     // column id: u0*n+u1 (d=3), u0 (d=2), 0 (d=1)
+  int32_t count;   // nodes in the run
+  int64_t begin;   // first sorted node
+};
+
+// Sorted nodes of one window on one side (sources or targets).
+struct SortedSide {
+  int64_t N = 0;
+  double* nx = nullptr;      // [d][N]: n * scaled coordinate, sorted by cell
+  int32_t* perm = nullptr;   // [N]: sorted position -> original node index
+  Chunk* chunks = nullptr;   // device
+  int64_t nchunks = 0;
+  int chunk_cap = 0;
+};
+
+void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
+                       SortedSide* out);
+void free_sorted_side(SortedSide* s);
+void make_poly_table(int m, double b, PolyTable* t);
+
+// ---------------------------------------------------------------------------
+// device: per-dimension window values of one node in the 2m stencil order
+// ---------------------------------------------------------------------------
+template <int MM>
+__device__ __forceinline__ void poly_weights(double f, const PolyTable& T, double (&w)[2 * MM]) {
+  const bool refl = f > 0.5;
+  const double x = (refl ? __dsub_rn(1.0, f) : f) - 0.25;
+#pragma unroll
+  for (int i = 0; i < 2 * MM; ++i) {
+    double v = T.c[i][kPolyTerms - 1];
+#pragma unroll
+    for (int k = kPolyTerms - 2; k >= 0; --k) v = fma(v, x, T.c[i][k]);
+    w[i] = v;
+  }
+  if (refl) {
+#pragma unroll
+    for (int i = 0; i < MM; ++i) {
+      const double t = w[i];
+      w[i] = w[2 * MM - 1 - i];
+      w[2 * MM - 1 - i] = t;
+    }
+  }
+}
+
+// exact mirror of nfft.py:118-122 on the stencil of one node (dist = f + m-1-i)
+template <int MM>
+__device__ __forceinline__ void exact_weights(double f, double b, double (&w)[2 * MM]) {
+#pragma unroll
+  for (int i = 0; i < 2 * MM; ++i) w[i] = kb_window(f + (double)(MM - 1 - i), MM, b);
+}
+
+}  // namespace afs

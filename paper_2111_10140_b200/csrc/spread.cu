@@ -4,7 +4,10 @@
 // is accumulated into the window's L2-resident real grid with native fp64
 // global reductions (RED.E.ADD.F64).  alpha is real, so the reference's
 // complex grid has zero imaginary part and only the real grid is kept.
+#include <algorithm>
+
 #include "afs_internal.cuh"
+#include "sliding.cuh"
 
 namespace afs {
 
@@ -76,9 +79,48 @@ static void launch_spread_m(afs_plan* p, const Window& w, const double* alpha, i
   }
 }
 
+static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t lda, int R,
+                             cudaStream_t s) {
+  if (p->window_eval != 0) return false;
+  const Window& w = p->win[l];
+  const SortedSide& sv = *p->src_side[l];
+  const int rg = v2_rhs_group(w.d, p->m, R);
+  if (rg < 1) return false;
+  for (int r0 = 0; r0 < R; r0 += rg) {
+    const int nr = std::min(rg, R - r0);
+    const double* a = alpha + r0 * lda;
+    double* g = p->grids + r0 * p->grid_total;
+    bool ok = false;
+    switch (w.d) {
+      case 1: ok = launch_spread_v2<1>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+      case 2: ok = launch_spread_v2<2>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+      default: ok = launch_spread_v2<3>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+    }
+    if (!ok) return false;   // no sliding kernel for this (d, m): whole window via v1
+  }
+  return true;
+}
+
+int v2_rhs_group(int D, int m, int R) {
+  // mirrors Fits<> in sliding.cuh: LPL * 2m * RG <= 64 doubles, RG = 2 only for m <= 4
+  const int W = 2 * m;
+  const int lines = D == 3 ? W * W : (D == 2 ? W : 1);
+  int team = 1;
+  if (D != 1) {
+    team = 1;
+    while (team < lines && team < 32) team *= 2;
+  }
+  const int lpl = (lines + team - 1) / team;
+  if (lpl * W > 64) return 0;
+  if (R >= 2 && m <= 4 && lpl * W * 2 <= 64) return 2;
+  return 1;
+}
+
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
   AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * p->grid_total * R, s));
-  for (const Window& w : p->win) {
+  for (int l = 0; l < p->P; ++l) {
+    const Window& w = p->win[l];
+    if (spread_v2_window(p, l, alpha, lda, R, s)) continue;
     switch (p->m) {
       case 1: launch_spread_m<1>(p, w, alpha, lda, R, s); break;
       case 2: launch_spread_m<2>(p, w, alpha, lda, R, s); break;

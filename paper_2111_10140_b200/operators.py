@@ -144,7 +144,8 @@ def _as_matrix(A, name):
 class _Plan:
     """Owns one native plan (afs_plan*) and its staging buffers."""
 
-    def __init__(self, X, Z, feats, weights, kernel, config, profile, device, max_rhs):
+    def __init__(self, X, Z, feats, weights, kernel, config, profile, device, max_rhs,
+                 window_eval="poly"):
         torch = _torch()
         self.lib = _native.load()
         self.device = torch.device("cuda", device if device is not None else torch.cuda.current_device())
@@ -200,6 +201,10 @@ class _Plan:
         desc.cutoff = m
         desc.grid = n
         desc.max_rhs = self.max_rhs
+        if window_eval not in ("poly", "exact"):
+            raise ValidationError("window_eval must be 'poly' or 'exact'")
+        desc.window_eval = 0 if window_eval == "poly" else 1
+        self.window_eval = window_eval
         handle = ctypes.c_void_p()
         torch.cuda.synchronize(self.device)
         _native.check(self.lib.afs_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
@@ -309,7 +314,7 @@ class AnovaKernelOperator:
     """
 
     def __init__(self, X, windows, sigma, profile="default", targets=None, config=None, *,
-                 strict=True, weights=None, device=None, max_rhs=1):
+                 strict=True, weights=None, device=None, max_rhs=1, window_eval="poly"):
         X = _as_matrix(X, "sources")
         if strict:
             if not isinstance(windows, WindowSet):
@@ -338,7 +343,7 @@ class AnovaKernelOperator:
         self.n_sources = X.shape[0]
         self.n_targets = X.shape[0] if Z is None else Z.shape[0]
         self._plan = _Plan(X, Z, list(windows.windows), list(windows.weights), kernel, config,
-                           profile, device, max_rhs)
+                           profile, device, max_rhs, window_eval)
         self.operators = self._plan.windows
 
     def apply(self, alpha):
@@ -362,7 +367,7 @@ class FastsumOperator:
     """
 
     def __init__(self, kernel, config, sources, targets=None, profile="default", *, device=None,
-                 max_rhs=1):
+                 max_rhs=1, window_eval="poly"):
         if not isinstance(kernel, GaussianKernel):
             raise ValidationError("kernel must be a GaussianKernel")
         profile = resolve_profile(profile)
@@ -381,7 +386,8 @@ class FastsumOperator:
         self.config = config
         self.profile = profile
         self.dims = d
-        self._plan = _Plan(X, Z, [tuple(range(d))], [1.0], kernel, config, profile, device, max_rhs)
+        self._plan = _Plan(X, Z, [tuple(range(d))], [1.0], kernel, config, profile, device, max_rhs,
+                           window_eval)
         w = self._plan.windows[0]
         self.scale = w.scale
         self.center = w.center

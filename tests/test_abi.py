@@ -34,9 +34,9 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layouts_match_header():
-    # afs_window_desc: 4 + 12 + 24 + 8 + 8 + 8 = 64 bytes; afs_plan_desc: 72 bytes
+    # afs_window_desc: 4 + 12 + 24 + 8 + 8 + 8 = 64 bytes; afs_plan_desc: 80 bytes
     assert ctypes.sizeof(_native.WindowDesc) == 64
-    assert ctypes.sizeof(_native.PlanDesc) == 72
+    assert ctypes.sizeof(_native.PlanDesc) == 80
     assert ctypes.sizeof(_native.PlanInfo) == 40
 
 

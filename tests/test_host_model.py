@@ -16,7 +16,7 @@ from paper_2111_10140_b200 import (AccuracyProfile, GaussianKernel, Periodizatio
 from paper_2111_10140_b200.spectrum import window_multiplier
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
-from make_golden import FASTSUM_CASES, fastsum_inputs  # noqa: E402
+from cases import FASTSUM_CASES, fastsum_inputs  # noqa: E402
 
 
 def _stencil(xs, n, m, b):

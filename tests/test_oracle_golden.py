@@ -13,7 +13,7 @@ from oracle import fastsum_oracle as orc
 from paper_2111_10140_b200 import synthetic
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
-from make_golden import FASTSUM_CASES, fastsum_inputs  # noqa: E402
+from cases import FASTSUM_CASES, fastsum_inputs  # noqa: E402
 
 PROFILES = {"rough": (1.5, 3), "default": (2.0, 4), "fine": (2.0, 6)}
 
