@@ -81,6 +81,7 @@ struct afs_plan {
   int launches_per_apply = 0;
   // v2 geometry (window_eval == 0): per window, bin-sorted source / target nodes
   int window_eval = 0;                 // 0 polynomial window + sliding kernels, 1 exact mirror (v1)
+  int kb_tab = 0;                      // compile-time KB table id (kb_table_id)
   std::vector<afs::SortedSide*> src_side, tgt_side;
   afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
   bool profiling = false;

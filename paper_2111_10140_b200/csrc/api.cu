@@ -202,6 +202,7 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
     if (p->window_eval == 0) {
       p->poly = new PolyTable();
       make_poly_table(p->m, p->b, p->poly);
+      p->kb_tab = kb_table_id(p->M, p->n);
       p->src_side.assign(p->P, nullptr);
       p->tgt_side.assign(p->P, nullptr);
       for (int l = 0; l < p->P; ++l) {

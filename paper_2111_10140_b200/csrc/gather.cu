@@ -120,9 +120,9 @@ static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R
     double* o = out + r0 * ldo;
     bool ok = false;
     switch (w.d) {
-      case 1: ok = launch_gather_v2<1>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
-      case 2: ok = launch_gather_v2<2>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
-      default: ok = launch_gather_v2<3>(sv, w, p->n, p->m, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+      case 1: ok = launch_gather_v2<1>(sv, w, p->n, p->m, p->kb_tab, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+      case 2: ok = launch_gather_v2<2>(sv, w, p->n, p->m, p->kb_tab, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
+      default: ok = launch_gather_v2<3>(sv, w, p->n, p->m, p->kb_tab, *p->poly, g, p->grid_total, nr, o, ldo, s); break;
     }
     if (!ok) {
       if (r0 != 0) throw Error(AFS_ERR_CUDA, "inconsistent v2 gather dispatch");

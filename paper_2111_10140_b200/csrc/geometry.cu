@@ -38,9 +38,13 @@ __global__ void k_permute_nodes(const double* __restrict__ nx_in, const int32_t*
 
 __global__ void k_column_counts(const uint64_t* __restrict__ key, int64_t N, uint64_t n,
                                 int32_t* __restrict__ counts) {
+  // keys are sorted, so a warp mostly sees one column: aggregate before the atomic
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  atomicAdd(&counts[key[i] / n], 1);
+  const bool live = i < N;
+  const unsigned long long col = live ? key[i] / n : ~0ULL;
+  const unsigned peers = __match_any_sync(0xffffffffu, col);
+  const int leader = __ffs(peers) - 1;
+  if (live && (int)(threadIdx.x & 31) == leader) atomicAdd(&counts[col], __popc(peers));
 }
 
 static int chunk_cap_for(int d) {
@@ -115,6 +119,12 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
     throw;
   }
   cleanup();
+}
+
+int kb_table_id(int M, int n) {
+  if (n == 2 * M) return 1;
+  if (2 * n == 3 * M) return 2;
+  return 0;
 }
 
 void free_sorted_side(SortedSide* s) {

@@ -7,6 +7,8 @@
 
 namespace afs {
 
+#include "kb_tables.inc"
+
 constexpr int kPolyMaxOffsets = 2 * AFS_MAX_CUTOFF;   // 2m
 constexpr int kPolyTerms = 14;                        // degree 13 in x = f - 1/4
 
@@ -39,19 +41,23 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
                        SortedSide* out);
 void free_sorted_side(SortedSide* s);
 void make_poly_table(int m, double b, PolyTable* t);
+int kb_table_id(int M, int n);   // 1: n = 2M, 2: 2n = 3M, 0: run-time table
 
 // ---------------------------------------------------------------------------
 // device: per-dimension window values of one node in the 2m stencil order
 // ---------------------------------------------------------------------------
-template <int MM>
+// TAB 0: run-time table T (any n/M); TAB 1, 2: compile-time tables (kb_tables.inc) for
+// n/M = 2 and 3/2, whose coefficients stream from the constant bank.
+template <int MM, int TAB>
 __device__ __forceinline__ void poly_weights(double f, const PolyTable& T, double (&w)[2 * MM]) {
   const bool refl = f > 0.5;
   const double x = (refl ? __dsub_rn(1.0, f) : f) - 0.25;
 #pragma unroll
   for (int i = 0; i < 2 * MM; ++i) {
-    double v = T.c[i][kPolyTerms - 1];
+    double v = TAB == 0 ? T.c[i][kPolyTerms - 1] : kb_coef<TAB, MM>(i, kPolyTerms - 1);
 #pragma unroll
-    for (int k = kPolyTerms - 2; k >= 0; --k) v = fma(v, x, T.c[i][k]);
+    for (int k = kPolyTerms - 2; k >= 0; --k)
+      v = fma(v, x, TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k));
     w[i] = v;
   }
   if (refl) {

@@ -1,4 +1,4 @@
-// v2 spread / gather: register sliding windows over bin-sorted nodes.
+// Spread / gather over bin-sorted nodes with register sliding windows.
 //
 // Nodes of a window are sorted by base cell (row-major, last dimension
 // fastest) and cut into column runs (Chunk).  A "team" of TEAM lanes takes
@@ -8,10 +8,11 @@
 // (gather) in registers; cell c lives in slot c mod 2m, so advancing the
 // window never moves registers: leaving cells are flushed (spread:
 // RED.E.ADD.F64 into the L2-resident grid) and entering cells loaded
-// (gather).  Per node, one lane evaluates the 2m*d window values once
-// (degree-13 polynomial, geometry.cuh) and stages them in shared memory;
-// the last dimension's values are stored pre-rotated into slot order so the
-// inner loop is a fixed, fully unrolled FMA sequence.
+// (gather; the cell one step ahead is prefetched so the common one-cell
+// advance never waits on L2).  Per node, one lane evaluates the 2m*d window
+// values once (degree-13 polynomial, geometry.cuh) and stages them in shared
+// memory; the last dimension's values are stored pre-rotated into slot order
+// so the per-node work is a fixed, fully unrolled FMA sequence.
 //
 // Reference: the spread is nfft.py:241-245 (bincount of alpha * prod_t w_t),
 // the gather nfft.py:228-229 ((g[flat] * w).sum(axis=1)), both over the
@@ -28,7 +29,9 @@ template <int D, int MM>
 struct Cfg {
   static constexpr int W = 2 * MM;
   static constexpr int LINES = D == 3 ? W * W : (D == 2 ? W : 1);
-  static constexpr int TEAM = D == 1 ? 1 : (LINES >= 32 ? 32 : (LINES > 16 ? 32 : (LINES > 8 ? 16 : (LINES > 4 ? 8 : (LINES > 2 ? 4 : (LINES > 1 ? 2 : 1))))));
+  static constexpr int TEAM =
+      D == 1 ? 1
+             : (LINES > 16 ? 32 : (LINES > 8 ? 16 : (LINES > 4 ? 8 : (LINES > 2 ? 4 : (LINES > 1 ? 2 : 1)))));
   static constexpr int LPL = (LINES + TEAM - 1) / TEAM;
   static constexpr int TPW = 32 / TEAM;
 };
@@ -38,17 +41,34 @@ struct Fits {
   static constexpr bool value = Cfg<D, MM>::LPL * Cfg<D, MM>::W * RG <= 64;
 };
 
+// staging row strides: S = 2 (mod 4) doubles keeps per-lane STS.128 conflict-free and
+// keeps every even offset 16-byte aligned
+__host__ __device__ constexpr int pad_stride(int s) { return s + ((6 - (s & 3)) & 3); }
+
+template <int D, int MM, int EXTRA>
+struct Stage {
+  static constexpr int W = 2 * MM;
+  static constexpr int STRIDE = pad_stride(D * W + EXTRA);            // per node
+  static constexpr int TEAM_SPAN = Cfg<D, MM>::TEAM * STRIDE + 2;     // per team (+2: bank skew)
+  static constexpr int WARP_SPAN = Cfg<D, MM>::TPW * TEAM_SPAN;
+  static constexpr int U_OFF = D * W;                                 // int bits of the base cell
+  static constexpr int A_OFF = D * W + 1;                             // alpha values (spread)
+};
+
+// c lies in [-n, 2n): the stencil never reaches further than m < n cells outside
 __device__ __forceinline__ int wrap_cell(int c, int n) {
-  c %= n;
-  return c < 0 ? c + n : c;
+  return c < 0 ? c + n : (c >= n ? c - n : c);
 }
 
-// slot k of a window whose first cell is lo holds cell lo + ((k - lo) mod W)
+// (k - lo) mod W for compile-time W
 template <int W>
-__device__ __forceinline__ int slot_cell(int k, int lo) {
-  int off = (k - lo) % W;
-  if (off < 0) off += W;
-  return lo + off;
+__device__ __forceinline__ int slot_rel(int k, int lo) {
+  if constexpr ((W & (W - 1)) == 0) {
+    return (k - lo) & (W - 1);
+  } else {
+    int off = (k - lo) % W;
+    return off < 0 ? off + W : off;
+  }
 }
 
 struct LineGeom {
@@ -58,7 +78,8 @@ struct LineGeom {
 };
 
 template <int D, int MM>
-__device__ __forceinline__ void line_geometry(int tl, int col, int n, LineGeom (&lg)[Cfg<D, MM>::LPL]) {
+__device__ __forceinline__ void line_geometry(int tl, int col, int n,
+                                              LineGeom (&lg)[Cfg<D, MM>::LPL]) {
   using C = Cfg<D, MM>;
   int ub0 = 0, ub1 = 0;
   if (D == 3) {
@@ -87,35 +108,48 @@ __device__ __forceinline__ void line_geometry(int tl, int col, int n, LineGeom (
   }
 }
 
-// Stage one node: window values of all dims (last dim rotated to slot order) + base.
-template <int D, int MM>
-__device__ __forceinline__ int stage_node(const SortedSide& sv, int64_t i, int n, const PolyTable& T,
-                                          double* row) {
+// prefetched per-node inputs of the next staging round
+template <int D>
+struct NodeIn {
+  double nx[D];
+  int perm;
+};
+
+template <int D>
+__device__ __forceinline__ void load_node(const SortedSide& sv, int64_t i, NodeIn<D>& in) {
+#pragma unroll
+  for (int t = 0; t < D; ++t) in.nx[t] = __ldcs(sv.nx + t * sv.N + i);   // streamed once
+  in.perm = __ldcs(sv.perm + i);
+}
+
+// Stage one node: window values of all dims (last dim rotated to slot order) + base cell.
+template <int D, int MM, int EXTRA, int TAB>
+__device__ __forceinline__ void stage_node(const NodeIn<D>& in, int n, const PolyTable& T,
+                                           double* row) {
   constexpr int W = 2 * MM;
-  int u = 0;
 #pragma unroll
   for (int t = 0; t < D; ++t) {
-    const double nx = sv.nx[t * sv.N + i];
+    const double nx = in.nx[t];
     const double fl = floor(nx);
-    const double f = nx - fl;                 // exact (Sterbenz)
+    const double f = nx - fl;                 // exact
     double wt[W];
-    poly_weights<MM>(f, T, wt);
+    poly_weights<MM, TAB>(f, T, wt);
     if (t < D - 1) {
 #pragma unroll
-      for (int o = 0; o < W; ++o) row[t * W + o] = wt[o];
+      for (int o = 0; o < W; o += 2)
+        *reinterpret_cast<double2*>(row + t * W + o) = make_double2(wt[o], wt[o + 1]);
     } else {
-      long long ul = (long long)fl % n;
-      u = (int)(ul < 0 ? ul + n : ul);
-      const int rot = (u + MM + 1) % W;
+      const int u = wrap_cell((int)fl, n);
+      const int rot = slot_rel<W>(u + MM + 1, 0);
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         int s = rot + o;
         s = s >= W ? s - W : s;
         row[(D - 1) * W + s] = wt[o];
       }
+      row[Stage<D, MM, EXTRA>::U_OFF] = __longlong_as_double((long long)u);
     }
   }
-  return u;
 }
 
 template <int D, int MM>
@@ -123,6 +157,16 @@ __device__ __forceinline__ double line_weight(const double* row, const LineGeom&
   if (D == 3) return g.valid ? row[g.a] * row[Cfg<D, MM>::W + g.b] : 0.0;
   if (D == 2) return g.valid ? row[g.a] : 0.0;
   return 1.0;
+}
+
+template <int W>
+__device__ __forceinline__ void load_last(const double* row_last, double (&wl)[W]) {
+#pragma unroll
+  for (int k = 0; k < W; k += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(row_last + k);
+    wl[k] = v.x;
+    wl[k + 1] = v.y;
+  }
 }
 
 __device__ __forceinline__ int warp_max(int v) {
@@ -134,19 +178,19 @@ __device__ __forceinline__ int warp_max(int v) {
 // ----------------------------------------------------------------------------
 // spread
 // ----------------------------------------------------------------------------
-template <int D, int MM, int RG>
+template <int D, int MM, int RG, int TAB>
 __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Window w, int n,
                                                    const PolyTable T,
                                                    const double* __restrict__ alpha, int64_t lda,
                                                    int nr, double* __restrict__ grid,
                                                    int64_t rhs_stride) {
   using C = Cfg<D, MM>;
+  using S = Stage<D, MM, 1 + RG>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
-  constexpr int STRIDE = D * W + RG + 1;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
   const int team = lane / TEAM, tl = lane - team * TEAM;
-  double* st = sm + (size_t)(threadIdx.x >> 5) * 32 * STRIDE + (size_t)team * TEAM * STRIDE;
+  double* st = sm + (size_t)(threadIdx.x >> 5) * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ci = gwarp * TPW + team;
   const bool active = ci < sv.nchunks;
@@ -164,22 +208,22 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
 #pragma unroll
       for (int r = 0; r < RG; ++r) acc[j][k][r] = 0.0;
 
-  auto flush = [&](int lo, int keep_from) {
-    // flush slots whose cell (window starting at lo) is < keep_from
+  // flush the slots of the window starting at cell lo whose offset from lo is < nleave
+  auto flush = [&](int lo, int nleave) {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      const int c = slot_cell<W>(k, lo);
-      if (c < keep_from) {
-        const int cm = wrap_cell(c, n);
+      const int rel = slot_rel<W>(k, lo);
+      if (rel < nleave) {
+        const int cm = wrap_cell(lo + rel, n);
 #pragma unroll
         for (int j = 0; j < LPL; ++j) {
           if (lg[j].valid) {
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
+            for (int r = 0; r < RG; ++r)
               if (r < nr) atomicAdd(g + r * rhs_stride + lg[j].off + cm, acc[j][k][r]);
-              acc[j][k][r] = 0.0;
-            }
           }
+#pragma unroll
+          for (int r = 0; r < RG; ++r) acc[j][k][r] = 0.0;
         }
       }
     }
@@ -187,34 +231,38 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
 
   int cur = INT_MIN;
   const int rounds = warp_max(ch.count);
+  NodeIn<D> nxt;
+  if (active && tl < ch.count) load_node<D>(sv, ch.begin + tl, nxt);
   for (int b0 = 0; b0 < rounds; b0 += TEAM) {
-    if (active && b0 + tl < ch.count) {
-      const int64_t i = ch.begin + b0 + tl;
-      double* row = st + tl * STRIDE;
-      const int u = stage_node<D, MM>(sv, i, n, T, row);
-      const int jj = sv.perm[i];
+    const bool mine = active && b0 + tl < ch.count;
+    if (mine) {
+      const NodeIn<D> in = nxt;
+      double a[RG];
 #pragma unroll
-      for (int r = 0; r < RG; ++r) row[D * W + r] = r < nr ? __ldg(alpha + r * lda + jj) : 0.0;
-      row[D * W + RG] = (double)u;
+      for (int r = 0; r < RG; ++r) a[r] = r < nr ? __ldg(alpha + r * lda + in.perm) : 0.0;
+      if (b0 + TEAM + tl < ch.count) load_node<D>(sv, ch.begin + b0 + TEAM + tl, nxt);
+      double* row = st + tl * S::STRIDE;
+      stage_node<D, MM, 1 + RG, TAB>(in, n, T, row);
+#pragma unroll
+      for (int r = 0; r < RG; ++r) row[S::A_OFF + r] = a[r];
     }
     __syncwarp();
     const int cnt = active ? min(TEAM, ch.count - b0) : 0;
     for (int q = 0; q < cnt; ++q) {
-      const double* row = st + q * STRIDE;
-      const int u = (int)row[D * W + RG];
+      const double* row = st + q * S::STRIDE;
+      const int u = (int)__double_as_longlong(row[S::U_OFF]);
       if (u != cur) {
-        if (cur != INT_MIN) flush(cur - MM + 1, u - MM + 1);
+        if (cur != INT_MIN) flush(cur - MM + 1, u - cur);
         cur = u;
       }
       double wl[W];
-#pragma unroll
-      for (int k = 0; k < W; ++k) wl[k] = row[(D - 1) * W + k];
+      load_last<W>(row + (D - 1) * W, wl);
 #pragma unroll
       for (int j = 0; j < LPL; ++j) {
         const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
         for (int r = 0; r < RG; ++r) {
-          const double p = lw * row[D * W + r];
+          const double p = lw * row[S::A_OFF + r];
 #pragma unroll
           for (int k = 0; k < W; ++k) acc[j][k][r] = fma(p, wl[k], acc[j][k][r]);
         }
@@ -222,28 +270,33 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
     }
     __syncwarp();
   }
-  if (active && cur != INT_MIN) flush(cur - MM + 1, INT_MAX);
+  if (active && cur != INT_MIN) flush(cur - MM + 1, W);
 }
 
 // ----------------------------------------------------------------------------
 // gather: out[perm] += eta * interp
 // ----------------------------------------------------------------------------
-template <int D, int MM, int RG>
+template <int TEAM>
+struct Red {
+  static constexpr int RSTR = TEAM == 1 ? 1 : (TEAM + 2);   // even, RSTR/2 odd for TEAM >= 4
+};
+
+template <int D, int MM, int RG, int TAB>
 __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Window w, int n,
                                                    const PolyTable T,
                                                    const double* __restrict__ grid,
                                                    int64_t rhs_stride, int nr,
                                                    double* __restrict__ out, int64_t ldo) {
   using C = Cfg<D, MM>;
+  using S = Stage<D, MM, 1>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
-  constexpr int STRIDE = D * W + 1;
-  constexpr int RSTR = TEAM + 1;               // padded reduction row
+  constexpr int RSTR = Red<TEAM>::RSTR;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int team = lane / TEAM, tl = lane - team * TEAM;
-  double* st = sm + (size_t)wib * 32 * STRIDE + (size_t)team * TEAM * STRIDE;
-  double* red = sm + (size_t)(blockDim.x >> 5) * 32 * STRIDE +
+  double* st = sm + (size_t)wib * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
+  double* red = sm + (size_t)(blockDim.x >> 5) * S::WARP_SPAN +
                 ((size_t)wib * TPW + team) * (size_t)TEAM * RSTR * RG;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ci = gwarp * TPW + team;
@@ -255,41 +308,62 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   const double* g = grid + w.grid_off;
 
   double gv[LPL][W][RG];
+  double ahead[LPL][RG];   // grid values of cell cur + MM + 1 (prefetched)
   int cur = INT_MIN;
+  auto load_cell = [&](int c, int j, int r) -> double {
+    return (lg[j].valid && r < nr) ? __ldg(g + r * rhs_stride + lg[j].off + wrap_cell(c, n)) : 0.0;
+  };
+
   const int rounds = warp_max(ch.count);
+  NodeIn<D> nxt;
+  if (active && tl < ch.count) load_node<D>(sv, ch.begin + tl, nxt);
   for (int b0 = 0; b0 < rounds; b0 += TEAM) {
+    const bool mine = active && b0 + tl < ch.count;
     int my_perm = -1;
-    if (active && b0 + tl < ch.count) {
-      const int64_t i = ch.begin + b0 + tl;
-      double* row = st + tl * STRIDE;
-      const int u = stage_node<D, MM>(sv, i, n, T, row);
-      row[D * W] = (double)u;
-      my_perm = sv.perm[i];
+    if (mine) {
+      const NodeIn<D> in = nxt;
+      my_perm = in.perm;
+      if (b0 + TEAM + tl < ch.count) load_node<D>(sv, ch.begin + b0 + TEAM + tl, nxt);
+      stage_node<D, MM, 1, TAB>(in, n, T, st + tl * S::STRIDE);
     }
     __syncwarp();
     const int cnt = active ? min(TEAM, ch.count - b0) : 0;
     for (int q = 0; q < cnt; ++q) {
-      const double* row = st + q * STRIDE;
-      const int u = (int)row[D * W];
+      const double* row = st + q * S::STRIDE;
+      const int u = (int)__double_as_longlong(row[S::U_OFF]);
       if (u != cur) {
         const int lo = u - MM + 1;
+        if (u == cur + 1) {
+          // one-cell advance: the entering cell u + MM was prefetched
+          const int k = slot_rel<W>(u + MM, 0);
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const int c = slot_cell<W>(k, lo);
-          if (cur == INT_MIN || c > cur + MM) {
-            const int cm = wrap_cell(c, n);
+          for (int kk = 0; kk < W; ++kk)
+            if (kk == k) {
 #pragma unroll
-            for (int j = 0; j < LPL; ++j)
+              for (int j = 0; j < LPL; ++j)
 #pragma unroll
-              for (int r = 0; r < RG; ++r)
-                gv[j][k][r] = (lg[j].valid && r < nr) ? __ldg(g + r * rhs_stride + lg[j].off + cm) : 0.0;
+                for (int r = 0; r < RG; ++r) gv[j][kk][r] = ahead[j][r];
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            const int c = lo + slot_rel<W>(k, lo);
+            if (cur == INT_MIN || c > cur + MM) {
+#pragma unroll
+              for (int j = 0; j < LPL; ++j)
+#pragma unroll
+                for (int r = 0; r < RG; ++r) gv[j][k][r] = load_cell(c, j, r);
+            }
           }
         }
         cur = u;
+#pragma unroll
+        for (int j = 0; j < LPL; ++j)
+#pragma unroll
+          for (int r = 0; r < RG; ++r) ahead[j][r] = load_cell(u + MM + 1, j, r);
       }
       double wl[W];
-#pragma unroll
-      for (int k = 0; k < W; ++k) wl[k] = row[(D - 1) * W + k];
+      load_last<W>(row + (D - 1) * W, wl);
       double part[RG];
 #pragma unroll
       for (int r = 0; r < RG; ++r) part[r] = 0.0;
@@ -298,24 +372,46 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
         const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
         for (int r = 0; r < RG; ++r) {
-          double s = 0.0;
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < W; ++k) s = fma(wl[k], gv[j][k][r], s);
-          part[r] = fma(lw, s, part[r]);
+          for (int k = 0; k < W; k += 2) {
+            s0 = fma(wl[k], gv[j][k][r], s0);
+            if (k + 1 < W) s1 = fma(wl[k + 1], gv[j][k + 1][r], s1);
+          }
+          part[r] = fma(lw, s0 + s1, part[r]);
         }
       }
+      if (TEAM == 1) {
 #pragma unroll
-      for (int r = 0; r < RG; ++r) red[(r * TEAM + q) * RSTR + tl] = part[r];
+        for (int r = 0; r < RG; ++r) red[r] = part[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < RG; ++r) red[(r * TEAM + q) * RSTR + tl] = part[r];
+      }
     }
     __syncwarp();
     if (my_perm >= 0) {
 #pragma unroll
       for (int r = 0; r < RG; ++r) {
         if (r < nr) {
-          const double* rr = red + (r * TEAM + tl) * RSTR;
-          double s = 0.0;
+          double s;
+          if (TEAM == 1) {
+            s = red[r];
+          } else {
+            const double* rr = red + (r * TEAM + tl) * RSTR;
+            double v[TEAM];
 #pragma unroll
-          for (int k = 0; k < TEAM; ++k) s += rr[k];
+            for (int k = 0; k < TEAM; k += 2) {
+              const double2 x = *reinterpret_cast<const double2*>(rr + k);
+              v[k] = x.x;
+              v[k + 1] = x.y;
+            }
+#pragma unroll
+            for (int h = TEAM / 2; h >= 1; h >>= 1)
+#pragma unroll
+              for (int k = 0; k < h; ++k) v[k] += v[k + h];
+            s = v[0];
+          }
           double* o = out + r * ldo + my_perm;
           *o = __dadd_rn(*o, __dmul_rn(w.eta, s));
         }
@@ -327,11 +423,11 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
 
 // host-side launchers (instantiated per dimension in sliding_d{1,2,3}.cu)
 template <int D>
-bool launch_spread_v2(const SortedSide& sv, const Window& w, int n, int m, const PolyTable& T,
+bool launch_spread_v2(const SortedSide& sv, const Window& w, int n, int m, int tab, const PolyTable& T,
                       const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
                       cudaStream_t s);
 template <int D>
-bool launch_gather_v2(const SortedSide& sv, const Window& w, int n, int m, const PolyTable& T,
+bool launch_gather_v2(const SortedSide& sv, const Window& w, int n, int m, int tab, const PolyTable& T,
                       const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                       cudaStream_t s);
 int v2_rhs_group(int D, int m, int R);

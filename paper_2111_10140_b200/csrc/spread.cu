@@ -92,9 +92,9 @@ static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t ld
     double* g = p->grids + r0 * p->grid_total;
     bool ok = false;
     switch (w.d) {
-      case 1: ok = launch_spread_v2<1>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
-      case 2: ok = launch_spread_v2<2>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
-      default: ok = launch_spread_v2<3>(sv, w, p->n, p->m, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+      case 1: ok = launch_spread_v2<1>(sv, w, p->n, p->m, p->kb_tab, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+      case 2: ok = launch_spread_v2<2>(sv, w, p->n, p->m, p->kb_tab, *p->poly, a, lda, nr, g, p->grid_total, s); break;
+      default: ok = launch_spread_v2<3>(sv, w, p->n, p->m, p->kb_tab, *p->poly, a, lda, nr, g, p->grid_total, s); break;
     }
     if (!ok) return false;   // no sliding kernel for this (d, m): whole window via v1
   }
