@@ -248,25 +248,31 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
     }
     __syncwarp();
     const int cnt = active ? min(TEAM, ch.count - b0) : 0;
-    for (int q = 0; q < cnt; ++q) {
-      const double* row = st + q * S::STRIDE;
-      const int u = (int)__double_as_longlong(row[S::U_OFF]);
+    int q = 0;
+    int u = cnt > 0 ? (int)__double_as_longlong(st[S::U_OFF]) : 0;
+    while (q < cnt) {
+      // window move (rare), then a branch-free run of nodes sharing base cell u
       if (u != cur) {
         if (cur != INT_MIN) flush(cur - MM + 1, u - cur);
         cur = u;
       }
-      double wl[W];
-      load_last<W>(row + (D - 1) * W, wl);
+      do {
+        const double* row = st + q * S::STRIDE;
+        ++q;
+        u = q < cnt ? (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) : INT_MIN;
+        double wl[W];
+        load_last<W>(row + (D - 1) * W, wl);
 #pragma unroll
-      for (int j = 0; j < LPL; ++j) {
-        const double lw = line_weight<D, MM>(row, lg[j]);
+        for (int j = 0; j < LPL; ++j) {
+          const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          const double p = lw * row[S::A_OFF + r];
+          for (int r = 0; r < RG; ++r) {
+            const double p = lw * row[S::A_OFF + r];
 #pragma unroll
-          for (int k = 0; k < W; ++k) acc[j][k][r] = fma(p, wl[k], acc[j][k][r]);
+            for (int k = 0; k < W; ++k) acc[j][k][r] = fma(p, wl[k], acc[j][k][r]);
+          }
         }
-      }
+      } while (u == cur);
     }
     __syncwarp();
   }
@@ -328,9 +334,9 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
     }
     __syncwarp();
     const int cnt = active ? min(TEAM, ch.count - b0) : 0;
-    for (int q = 0; q < cnt; ++q) {
-      const double* row = st + q * S::STRIDE;
-      const int u = (int)__double_as_longlong(row[S::U_OFF]);
+    int q = 0;
+    int u = cnt > 0 ? (int)__double_as_longlong(st[S::U_OFF]) : 0;
+    while (q < cnt) {
       if (u != cur) {
         const int lo = u - MM + 1;
         if (u == cur + 1) {
@@ -362,32 +368,37 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
 #pragma unroll
           for (int r = 0; r < RG; ++r) ahead[j][r] = load_cell(u + MM + 1, j, r);
       }
-      double wl[W];
-      load_last<W>(row + (D - 1) * W, wl);
-      double part[RG];
+      do {
+        const double* row = st + q * S::STRIDE;
+        const int qq = q++;
+        u = q < cnt ? (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) : INT_MIN;
+        double wl[W];
+        load_last<W>(row + (D - 1) * W, wl);
+        double part[RG];
 #pragma unroll
-      for (int r = 0; r < RG; ++r) part[r] = 0.0;
+        for (int r = 0; r < RG; ++r) part[r] = 0.0;
 #pragma unroll
-      for (int j = 0; j < LPL; ++j) {
-        const double lw = line_weight<D, MM>(row, lg[j]);
+        for (int j = 0; j < LPL; ++j) {
+          const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          double s0 = 0.0, s1 = 0.0;
+          for (int r = 0; r < RG; ++r) {
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < W; k += 2) {
-            s0 = fma(wl[k], gv[j][k][r], s0);
-            if (k + 1 < W) s1 = fma(wl[k + 1], gv[j][k + 1][r], s1);
+            for (int k = 0; k < W; k += 2) {
+              s0 = fma(wl[k], gv[j][k][r], s0);
+              if (k + 1 < W) s1 = fma(wl[k + 1], gv[j][k + 1][r], s1);
+            }
+            part[r] = fma(lw, s0 + s1, part[r]);
           }
-          part[r] = fma(lw, s0 + s1, part[r]);
         }
-      }
-      if (TEAM == 1) {
+        if (TEAM == 1) {
 #pragma unroll
-        for (int r = 0; r < RG; ++r) red[r] = part[r];
-      } else {
+          for (int r = 0; r < RG; ++r) red[r] = part[r];
+        } else {
 #pragma unroll
-        for (int r = 0; r < RG; ++r) red[(r * TEAM + q) * RSTR + tl] = part[r];
-      }
+          for (int r = 0; r < RG; ++r) red[(r * TEAM + qq) * RSTR + tl] = part[r];
+        }
+      } while (u == cur);
     }
     __syncwarp();
     if (my_perm >= 0) {
