@@ -45,11 +45,16 @@ struct Fits {
 // keeps every even offset 16-byte aligned
 __host__ __device__ constexpr int pad_stride(int s) { return s + ((6 - (s & 3)) & 3); }
 
+template <int D>
+struct NodesPerLane;
+
 template <int D, int MM, int EXTRA>
 struct Stage {
   static constexpr int W = 2 * MM;
+  static constexpr int P = NodesPerLane<D>::P;                        // nodes per lane per round
+  static constexpr int BATCH = Cfg<D, MM>::TEAM * P;                  // nodes per team per round
   static constexpr int STRIDE = pad_stride(D * W + EXTRA);            // per node
-  static constexpr int TEAM_SPAN = Cfg<D, MM>::TEAM * STRIDE + 2;     // per team (+2: bank skew)
+  static constexpr int TEAM_SPAN = BATCH * STRIDE + 2;                // per team (+2: bank skew)
   static constexpr int WARP_SPAN = Cfg<D, MM>::TPW * TEAM_SPAN;
   static constexpr int U_OFF = D * W;                                 // int bits of the base cell
   static constexpr int A_OFF = D * W + 1;                             // alpha values (spread)
@@ -122,32 +127,80 @@ __device__ __forceinline__ void load_node(const SortedSide& sv, int64_t i, NodeI
   in.perm = __ldcs(sv.perm + i);
 }
 
-// Stage one node: window values of all dims (last dim rotated to slot order) + base cell.
+// Nodes staged per lane per round: the Horner evaluations of all P nodes x D dims
+// share each coefficient (a double constant costs two MOVs to materialise).
+template <int D>
+struct NodesPerLane {
+  static constexpr int P = D == 3 ? 1 : (D == 2 ? 2 : 4);
+};
+
+// one staging round: lane tl stages nodes tl + TEAM*p (p < P) of the batch at b0
 template <int D, int MM, int EXTRA, int TAB>
-__device__ __forceinline__ void stage_node(const NodeIn<D>& in, int n, const PolyTable& T,
-                                           double* row) {
+struct Round {
+  using S = Stage<D, MM, EXTRA>;
+  static constexpr int P = S::P, TEAM = Cfg<D, MM>::TEAM;
+  NodeIn<D> nxt[P];
+
+  __device__ __forceinline__ void prefetch(const SortedSide& sv, const Chunk& ch, bool active,
+                                           int tl, int b0) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int q = b0 + tl + TEAM * p;
+      if (active && q < ch.count) load_node<D>(sv, ch.begin + q, nxt[p]);
+    }
+  }
+};
+
+// Stage P nodes: window values of all dims (last dim rotated to slot order) + base cell.
+// Values for f > 1/2 come from the mirrored polynomial (geometry.cuh) and are written to
+// the mirrored stencil position.
+template <int D, int MM, int EXTRA, int TAB, int P>
+__device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool (&live)[P], int n,
+                                            const PolyTable& T, double* const (&row)[P]) {
   constexpr int W = 2 * MM;
+  double x[P][D];
+  int pos0[P][D];   // store position of offset 0; step +1 or -1 (mirrored)
+  int step[P][D];
 #pragma unroll
-  for (int t = 0; t < D; ++t) {
-    const double nx = in.nx[t];
-    const double fl = floor(nx);
-    const double f = nx - fl;                 // exact
-    double wt[W];
-    poly_weights<MM, TAB>(f, T, wt);
-    if (t < D - 1) {
+  for (int p = 0; p < P; ++p) {
 #pragma unroll
-      for (int o = 0; o < W; o += 2)
-        *reinterpret_cast<double2*>(row + t * W + o) = make_double2(wt[o], wt[o + 1]);
-    } else {
-      const int u = wrap_cell((int)fl, n);
-      const int rot = slot_rel<W>(u + MM + 1, 0);
-#pragma unroll
-      for (int o = 0; o < W; ++o) {
-        int s = rot + o;
-        s = s >= W ? s - W : s;
-        row[(D - 1) * W + s] = wt[o];
+    for (int t = 0; t < D; ++t) {
+      const double nx = in[p].nx[t];
+      const double fl = floor(nx);
+      const double f = nx - fl;   // exact
+      const bool refl = f > 0.5;
+      x[p][t] = (refl ? __dsub_rn(1.0, f) : f) - 0.25;
+      int base = 0;
+      if (t == D - 1) {
+        const int u = wrap_cell((int)fl, n);
+        base = slot_rel<W>(u + MM + 1, 0);   // slot of stencil offset 0
+        row[p][Stage<D, MM, EXTRA>::U_OFF] = __longlong_as_double((long long)u);
       }
-      row[Stage<D, MM, EXTRA>::U_OFF] = __longlong_as_double((long long)u);
+      pos0[p][t] = refl ? base + W - 1 : base;
+      step[p][t] = refl ? -1 : 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    double v[P][D];
+#pragma unroll
+    for (int k = kPolyTerms - 1; k >= 0; --k) {
+      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+#pragma unroll
+        for (int t = 0; t < D; ++t) v[p][t] = k == kPolyTerms - 1 ? c : fma(v[p][t], x[p][t], c);
+    }
+    // stores are unconditional (rows of dead nodes are never read) so that the compiler
+    // keeps all P*D evaluations together and shares each materialised coefficient
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        int s = pos0[p][t] + step[p][t] * i;   // in (-W, 2W)
+        if (t == D - 1) s = s >= W ? s - W : (s < 0 ? s + W : s);
+        row[p][t * W + s] = v[p][t];
+      }
     }
   }
 }
@@ -231,23 +284,35 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
 
   int cur = INT_MIN;
   const int rounds = warp_max(ch.count);
-  NodeIn<D> nxt;
-  if (active && tl < ch.count) load_node<D>(sv, ch.begin + tl, nxt);
-  for (int b0 = 0; b0 < rounds; b0 += TEAM) {
-    const bool mine = active && b0 + tl < ch.count;
-    if (mine) {
-      const NodeIn<D> in = nxt;
-      double a[RG];
+  constexpr int P = S::P, BATCH = S::BATCH;
+  Round<D, MM, 1 + RG, TAB> rd;
+  rd.prefetch(sv, ch, active, tl, 0);
+  for (int b0 = 0; b0 < rounds; b0 += BATCH) {
+    {
+      NodeIn<D> in[P];
+      bool live[P];
+      double* rows[P];
+      double a[P][RG];
 #pragma unroll
-      for (int r = 0; r < RG; ++r) a[r] = r < nr ? __ldg(alpha + r * lda + in.perm) : 0.0;
-      if (b0 + TEAM + tl < ch.count) load_node<D>(sv, ch.begin + b0 + TEAM + tl, nxt);
-      double* row = st + tl * S::STRIDE;
-      stage_node<D, MM, 1 + RG, TAB>(in, n, T, row);
+      for (int p = 0; p < P; ++p) {
+        in[p] = rd.nxt[p];
+        live[p] = active && b0 + tl + TEAM * p < ch.count;
+        rows[p] = st + (tl + TEAM * p) * S::STRIDE;
 #pragma unroll
-      for (int r = 0; r < RG; ++r) row[S::A_OFF + r] = a[r];
+        for (int r = 0; r < RG; ++r)
+          a[p][r] = (live[p] && r < nr) ? __ldg(alpha + r * lda + in[p].perm) : 0.0;
+      }
+      rd.prefetch(sv, ch, active, tl, b0 + BATCH);
+      stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, T, rows);
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (live[p]) {
+#pragma unroll
+          for (int r = 0; r < RG; ++r) rows[p][S::A_OFF + r] = a[p][r];
+        }
     }
     __syncwarp();
-    const int cnt = active ? min(TEAM, ch.count - b0) : 0;
+    const int cnt = active ? min(BATCH, ch.count - b0) : 0;
     int q = 0;
     int u = cnt > 0 ? (int)__double_as_longlong(st[S::U_OFF]) : 0;
     while (q < cnt) {
@@ -302,8 +367,9 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   const int wib = threadIdx.x >> 5;
   const int team = lane / TEAM, tl = lane - team * TEAM;
   double* st = sm + (size_t)wib * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
+  constexpr int P = S::P, BATCH = S::BATCH;
   double* red = sm + (size_t)(blockDim.x >> 5) * S::WARP_SPAN +
-                ((size_t)wib * TPW + team) * (size_t)TEAM * RSTR * RG;
+                ((size_t)wib * TPW + team) * (size_t)BATCH * RSTR * RG;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ci = gwarp * TPW + team;
   const bool active = ci < sv.nchunks;
@@ -321,19 +387,26 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   };
 
   const int rounds = warp_max(ch.count);
-  NodeIn<D> nxt;
-  if (active && tl < ch.count) load_node<D>(sv, ch.begin + tl, nxt);
-  for (int b0 = 0; b0 < rounds; b0 += TEAM) {
-    const bool mine = active && b0 + tl < ch.count;
-    int my_perm = -1;
-    if (mine) {
-      const NodeIn<D> in = nxt;
-      my_perm = in.perm;
-      if (b0 + TEAM + tl < ch.count) load_node<D>(sv, ch.begin + b0 + TEAM + tl, nxt);
-      stage_node<D, MM, 1, TAB>(in, n, T, st + tl * S::STRIDE);
+  Round<D, MM, 1, TAB> rd;
+  rd.prefetch(sv, ch, active, tl, 0);
+  for (int b0 = 0; b0 < rounds; b0 += BATCH) {
+    int my_perm[P];
+    {
+      NodeIn<D> in[P];
+      bool live[P];
+      double* rows[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        in[p] = rd.nxt[p];
+        live[p] = active && b0 + tl + TEAM * p < ch.count;
+        rows[p] = st + (tl + TEAM * p) * S::STRIDE;
+        my_perm[p] = live[p] ? in[p].perm : -1;
+      }
+      rd.prefetch(sv, ch, active, tl, b0 + BATCH);
+      stage_nodes<D, MM, 1, TAB, P>(in, live, n, T, rows);
     }
     __syncwarp();
-    const int cnt = active ? min(TEAM, ch.count - b0) : 0;
+    const int cnt = active ? min(BATCH, ch.count - b0) : 0;
     int q = 0;
     int u = cnt > 0 ? (int)__double_as_longlong(st[S::U_OFF]) : 0;
     while (q < cnt) {
@@ -391,25 +464,23 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
             part[r] = fma(lw, s0 + s1, part[r]);
           }
         }
-        if (TEAM == 1) {
 #pragma unroll
-          for (int r = 0; r < RG; ++r) red[r] = part[r];
-        } else {
-#pragma unroll
-          for (int r = 0; r < RG; ++r) red[(r * TEAM + qq) * RSTR + tl] = part[r];
-        }
+        for (int r = 0; r < RG; ++r) red[(r * BATCH + qq) * RSTR + tl] = part[r];
       } while (u == cur);
     }
     __syncwarp();
-    if (my_perm >= 0) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (my_perm[p] < 0) continue;
+      const int qq = tl + TEAM * p;
 #pragma unroll
       for (int r = 0; r < RG; ++r) {
         if (r < nr) {
           double s;
           if (TEAM == 1) {
-            s = red[r];
+            s = red[r * BATCH + qq];
           } else {
-            const double* rr = red + (r * TEAM + tl) * RSTR;
+            const double* rr = red + (r * BATCH + qq) * RSTR;
             double v[TEAM];
 #pragma unroll
             for (int k = 0; k < TEAM; k += 2) {
@@ -423,7 +494,7 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
               for (int k = 0; k < h; ++k) v[k] += v[k + h];
             s = v[0];
           }
-          double* o = out + r * ldo + my_perm;
+          double* o = out + r * ldo + my_perm[p];
           *o = __dadd_rn(*o, __dmul_rn(w.eta, s));
         }
       }

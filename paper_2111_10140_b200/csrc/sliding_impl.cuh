@@ -29,7 +29,7 @@ static void run_gather_v2(const SortedSide& sv, const Window& w, int n, const Po
   constexpr int threads = 128;
   const size_t smem = (size_t)(threads / 32) *
                       (Stage<D, MM, 1>::WARP_SPAN +
-                       (size_t)C::TPW * C::TEAM * Red<C::TEAM>::RSTR * RG) *
+                       (size_t)C::TPW * Stage<D, MM, 1>::BATCH * Red<C::TEAM>::RSTR * RG) *
                       sizeof(double);
   const int64_t warps = (sv.nchunks + C::TPW - 1) / C::TPW;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
