@@ -48,12 +48,13 @@ __host__ __device__ constexpr int pad_stride(int s) { return s + ((6 - (s & 3)) 
 template <int D>
 struct NodesPerLane;
 
-template <int D, int MM, int EXTRA>
+template <int D, int MM, int EXTRA, int MIN_STRIDE = 0>
 struct Stage {
   static constexpr int W = 2 * MM;
   static constexpr int P = NodesPerLane<D>::P;                        // nodes per lane per round
   static constexpr int BATCH = Cfg<D, MM>::TEAM * P;                  // nodes per team per round
-  static constexpr int STRIDE = pad_stride(D * W + EXTRA);            // per node
+  static constexpr int STRIDE =                                       // per node
+      pad_stride(D * W + EXTRA > MIN_STRIDE ? D * W + EXTRA : MIN_STRIDE);
   static constexpr int TEAM_SPAN = BATCH * STRIDE + 2;                // per team (+2: bank skew)
   static constexpr int WARP_SPAN = Cfg<D, MM>::TPW * TEAM_SPAN;
   static constexpr int U_OFF = D * W;                                 // int bits of the base cell
@@ -359,17 +360,17 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
                                                    int64_t rhs_stride, int nr,
                                                    double* __restrict__ out, int64_t ldo) {
   using C = Cfg<D, MM>;
-  using S = Stage<D, MM, 1>;
+  constexpr int RSTR = Red<C::TEAM>::RSTR;
+  // a node's staging row is reused for its per-lane partial sums once it is processed
+  using S = Stage<D, MM, 1, RG * RSTR>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
-  constexpr int RSTR = Red<TEAM>::RSTR;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int team = lane / TEAM, tl = lane - team * TEAM;
+  const unsigned team_mask = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (team * TEAM));
   double* st = sm + (size_t)wib * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
   constexpr int P = S::P, BATCH = S::BATCH;
-  double* red = sm + (size_t)(blockDim.x >> 5) * S::WARP_SPAN +
-                ((size_t)wib * TPW + team) * (size_t)BATCH * RSTR * RG;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ci = gwarp * TPW + team;
   const bool active = ci < sv.nchunks;
@@ -464,8 +465,10 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
             part[r] = fma(lw, s0 + s1, part[r]);
           }
         }
+        __syncwarp(team_mask);   // every lane of the team is done reading row qq
+        double* prow = st + qq * S::STRIDE;
 #pragma unroll
-        for (int r = 0; r < RG; ++r) red[(r * BATCH + qq) * RSTR + tl] = part[r];
+        for (int r = 0; r < RG; ++r) prow[r * RSTR + tl] = part[r];
       } while (u == cur);
     }
     __syncwarp();
@@ -477,10 +480,10 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
       for (int r = 0; r < RG; ++r) {
         if (r < nr) {
           double s;
+          const double* rr = st + qq * S::STRIDE + r * RSTR;
           if (TEAM == 1) {
-            s = red[r * BATCH + qq];
+            s = rr[0];
           } else {
-            const double* rr = red + (r * BATCH + qq) * RSTR;
             double v[TEAM];
 #pragma unroll
             for (int k = 0; k < TEAM; k += 2) {

@@ -28,9 +28,7 @@ static void run_gather_v2(const SortedSide& sv, const Window& w, int n, const Po
   using C = Cfg<D, MM>;
   constexpr int threads = 128;
   const size_t smem = (size_t)(threads / 32) *
-                      (Stage<D, MM, 1>::WARP_SPAN +
-                       (size_t)C::TPW * Stage<D, MM, 1>::BATCH * Red<C::TEAM>::RSTR * RG) *
-                      sizeof(double);
+                      Stage<D, MM, 1, RG * Red<C::TEAM>::RSTR>::WARP_SPAN * sizeof(double);
   const int64_t warps = (sv.nchunks + C::TPW - 1) / C::TPW;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (smem > 48 * 1024)
