@@ -181,26 +181,31 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
       step[p][t] = refl ? -1 : 1;
     }
   }
+  // all W*P*D Horner chains advance together (k outer): W*P*D independent FMAs per step
+  // hide the DFMA latency, and each coefficient is materialised once for P*D uses
+  double v[W][P][D];
 #pragma unroll
-  for (int i = 0; i < W; ++i) {
-    double v[P][D];
+  for (int k = kPolyTerms - 1; k >= 0; --k) {
 #pragma unroll
-    for (int k = kPolyTerms - 1; k >= 0; --k) {
+    for (int i = 0; i < W; ++i) {
       const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
 #pragma unroll
       for (int p = 0; p < P; ++p)
 #pragma unroll
-        for (int t = 0; t < D; ++t) v[p][t] = k == kPolyTerms - 1 ? c : fma(v[p][t], x[p][t], c);
+        for (int t = 0; t < D; ++t)
+          v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
     }
-    // stores are unconditional (rows of dead nodes are never read) so that the compiler
-    // keeps all P*D evaluations together and shares each materialised coefficient
+  }
+  // stores are unconditional (rows of dead nodes are never read)
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
 #pragma unroll
       for (int t = 0; t < D; ++t) {
         int s = pos0[p][t] + step[p][t] * i;   // in (-W, 2W)
         if (t == D - 1) s = s >= W ? s - W : (s < 0 ? s + W : s);
-        row[p][t * W + s] = v[p][t];
+        row[p][t * W + s] = v[i][p][t];
       }
     }
   }
@@ -392,6 +397,7 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   rd.prefetch(sv, ch, active, tl, 0);
   for (int b0 = 0; b0 < rounds; b0 += BATCH) {
     int my_perm[P];
+    double prior[P][RG];   // out[perm] before this window, loaded early (random access)
     {
       NodeIn<D> in[P];
       bool live[P];
@@ -402,6 +408,9 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
         live[p] = active && b0 + tl + TEAM * p < ch.count;
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
         my_perm[p] = live[p] ? in[p].perm : -1;
+#pragma unroll
+        for (int r = 0; r < RG; ++r)
+          prior[p][r] = (live[p] && r < nr) ? out[r * ldo + in[p].perm] : 0.0;
       }
       rd.prefetch(sv, ch, active, tl, b0 + BATCH);
       stage_nodes<D, MM, 1, TAB, P>(in, live, n, T, rows);
@@ -497,8 +506,7 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
               for (int k = 0; k < h; ++k) v[k] += v[k + h];
             s = v[0];
           }
-          double* o = out + r * ldo + my_perm[p];
-          *o = __dadd_rn(*o, __dmul_rn(w.eta, s));
+          out[r * ldo + my_perm[p]] = __dadd_rn(prior[p][r], __dmul_rn(w.eta, s));
         }
       }
     }
