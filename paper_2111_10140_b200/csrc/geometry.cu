@@ -48,8 +48,9 @@ __global__ void k_column_counts(const uint64_t* __restrict__ key, int64_t N, uin
 }
 
 static int chunk_cap_for(int d) {
-  // one team of TEAM lanes per chunk; ~32 nodes per lane of work per chunk
-  return d == 3 ? 1024 : (d == 2 ? 256 : 32);
+  // d = 3: one 32-lane team per run; d <= 2: one warp per run, 32 nodes per lane
+  (void)d;
+  return 1024;
 }
 
 void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {

@@ -2,8 +2,29 @@
 #pragma once
 
 #include "sliding.cuh"
+#include "solo.cuh"
 
 namespace afs {
+
+template <int D, int MM, int RG, int TAB>
+static void run_spread_solo(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
+                            const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
+                            cudaStream_t s) {
+  constexpr int threads = 128;   // one warp per column run
+  const int64_t blocks = (sv.nchunks * 32 + threads - 1) / threads;
+  k_spread_solo<D, MM, RG, TAB><<<(unsigned)blocks, threads, 0, s>>>(sv, w, n, T, alpha, lda, nr,
+                                                                    grid, rs);
+}
+
+template <int D, int MM, int RG, int TAB>
+static void run_gather_solo(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
+                            const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
+                            cudaStream_t s) {
+  constexpr int threads = 128;
+  const int64_t blocks = (sv.nchunks * 32 + threads - 1) / threads;
+  k_gather_solo<D, MM, RG, TAB><<<(unsigned)blocks, threads, 0, s>>>(sv, w, n, T, grid, rs, nr,
+                                                                    out, ldo);
+}
 
 template <int D, int MM, int RG, int TAB>
 static void run_spread_v2(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
@@ -42,6 +63,18 @@ template <int D, int MM, int TAB>
 static bool spread_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
                        cudaStream_t s) {
+  if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
+    if (nr >= 2) {
+      run_spread_solo<D, MM, 2, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
+      return true;
+    }
+  }
+  if constexpr (SoloFits<D, MM, 1>::value) {
+    if (nr == 1) {
+      run_spread_solo<D, MM, 1, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
+      return true;
+    }
+  }
   if constexpr (Fits<D, MM, 2>::value && MM <= 4 && TAB != 0) {
     if (nr >= 2) {
       run_spread_v2<D, MM, 2, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
@@ -70,6 +103,18 @@ template <int D, int MM, int TAB>
 static bool gather_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                        cudaStream_t s) {
+  if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
+    if (nr >= 2) {
+      run_gather_solo<D, MM, 2, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);
+      return true;
+    }
+  }
+  if constexpr (SoloFits<D, MM, 1>::value) {
+    if (nr == 1) {
+      run_gather_solo<D, MM, 1, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);
+      return true;
+    }
+  }
   if constexpr (Fits<D, MM, 2>::value && MM <= 4 && TAB != 0) {
     if (nr >= 2) {
       run_gather_v2<D, MM, 2, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);

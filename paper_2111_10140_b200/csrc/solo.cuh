@@ -1,0 +1,301 @@
+// Spread / gather for 1-D and 2-D windows with lane-private sliding windows.
+//
+// A warp takes one column run (Chunk) of bin-sorted nodes; lane l processes
+// nodes begin + l + 32 k (coalesced loads, neighbouring lanes sit in the same
+// or the next cell).  Each lane owns the whole stencil: LINES = (2m)^(d-1)
+// lines x 2m cells of accumulators (spread) or grid values (gather) in
+// registers, in "shift" order (slot k <-> cell lo + k).  A window move by one
+// cell shifts the registers (rare: runs are sorted) and flushes / loads one
+// cell per line.  No shared memory and no cross-lane traffic per node.
+//
+// Spread epilogue: lanes first move to the warp's last cell (flushing what
+// leaves individually), then a transposed butterfly reduces the identical
+// windows across the warp so each lane issues only LINES*2m/32 RED.F64.
+//
+// Reference: nfft.py:241-245 (spread), nfft.py:228-229 (gather), stencil
+// nfft.py:164-188; window values as in geometry.cuh.
+#pragma once
+
+#include <climits>
+
+#include "sliding.cuh"
+
+namespace afs {
+
+template <int D, int MM>
+struct SoloCfg {
+  static constexpr int W = 2 * MM;
+  static constexpr int LINES = D == 2 ? W : 1;
+  static constexpr int NACC = LINES * W;
+};
+
+// window values of one node, dims 0..D-1 in stencil order
+template <int D, int MM, int TAB>
+__device__ __forceinline__ void solo_weights(const double (&nx)[D], const PolyTable& T,
+                                             double (&wt)[D][2 * MM], int& u_last, int n) {
+  constexpr int W = 2 * MM;
+  double x[D];
+  bool refl[D];
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const double fl = floor(nx[t]);
+    const double f = nx[t] - fl;
+    refl[t] = f > 0.5;
+    x[t] = (refl[t] ? __dsub_rn(1.0, f) : f) - 0.25;
+    if (t == D - 1) u_last = wrap_cell((int)fl, n);
+  }
+  double v[W][D];
+#pragma unroll
+  for (int k = kPolyTerms - 1; k >= 0; --k) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
+#pragma unroll
+      for (int t = 0; t < D; ++t) v[i][t] = k == kPolyTerms - 1 ? c : fma(v[i][t], x[t], c);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < D; ++t)
+#pragma unroll
+    for (int i = 0; i < W; ++i) wt[t][i] = refl[t] ? v[W - 1 - i][t] : v[i][t];
+}
+
+template <int D, int MM>
+__device__ __forceinline__ int64_t rowoff_dyn(int col, int ln, int n) {
+  return D == 2 ? (int64_t)wrap_cell(col - MM + 1 + ln, n) * n : 0;
+}
+
+template <int D, int MM, int RG>
+struct SoloFits {
+  static constexpr bool value = D <= 2 && SoloCfg<D, MM>::NACC * RG <= 64;
+};
+
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ----------------------------------------------------------------------------
+// spread
+// ----------------------------------------------------------------------------
+template <int D, int MM, int RG, int TAB>
+__global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const Window w, int n,
+                                                     const PolyTable T,
+                                                     const double* __restrict__ alpha,
+                                                     int64_t lda, int nr,
+                                                     double* __restrict__ grid,
+                                                     int64_t rhs_stride) {
+  using C = SoloCfg<D, MM>;
+  constexpr int W = C::W, LINES = C::LINES, NACC = C::NACC;
+  const int lane = threadIdx.x & 31;
+  const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ci >= sv.nchunks) return;   // warp-uniform
+  const Chunk ch = sv.chunks[ci];
+  double* g = grid + w.grid_off;
+  int64_t rowoff[LINES];
+#pragma unroll
+  for (int a = 0; a < LINES; ++a)
+    rowoff[a] = D == 2 ? (int64_t)wrap_cell(ch.col - MM + 1 + a, n) * n : 0;
+
+  double acc[LINES][W][RG];
+#pragma unroll
+  for (int a = 0; a < LINES; ++a)
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+#pragma unroll
+      for (int r = 0; r < RG; ++r) acc[a][k][r] = 0.0;
+
+  // flush slot 0 of every line (cell lo) and shift the window up by one cell
+  auto shift1 = [&](int lo) {
+    const int cm = wrap_cell(lo, n);
+#pragma unroll
+    for (int a = 0; a < LINES; ++a) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        if (r < nr && acc[a][0][r] != 0.0) atomicAdd(g + r * rhs_stride + rowoff[a] + cm, acc[a][0][r]);
+#pragma unroll
+        for (int k = 0; k + 1 < W; ++k) acc[a][k][r] = acc[a][k + 1][r];
+        acc[a][W - 1][r] = 0.0;
+      }
+    }
+  };
+  auto move_to = [&](int& cur, int u) {
+    // advance the window from base cell cur to u (> cur)
+    if (u - cur >= W) {
+#pragma unroll 1
+      for (int j = 0; j < W; ++j) shift1(cur - MM + 1 + j);
+    } else {
+#pragma unroll 1
+      for (int c = cur; c < u; ++c) shift1(c - MM + 1);
+    }
+    cur = u;
+  };
+
+  int cur = INT_MIN;
+  const int count = ch.count;
+  for (int q = lane; q < count; q += 32) {
+    const int64_t i = ch.begin + q;
+    double nx[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) nx[t] = __ldcs(sv.nx + t * sv.N + i);
+    const int j = __ldcs(sv.perm + i);
+    double a[RG];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) a[r] = r < nr ? __ldg(alpha + r * lda + j) : 0.0;
+    double wt[D][W];
+    int u;
+    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
+    if (cur == INT_MIN) cur = u;
+    if (u != cur) move_to(cur, u);
+#pragma unroll
+    for (int ln = 0; ln < LINES; ++ln) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        const double p = (D == 2 ? wt[0][ln] : 1.0) * a[r];
+#pragma unroll
+        for (int k = 0; k < W; ++k) acc[ln][k][r] = fma(p, wt[D - 1][k], acc[ln][k][r]);
+      }
+    }
+  }
+  // epilogue: align every lane's window to the warp's last base cell, then reduce
+  const bool has = cur != INT_MIN;
+  const int top = warp_max_i(has ? cur : INT_MIN);
+  if (top == INT_MIN) return;
+  if (has && cur < top) move_to(cur, top);
+  // transposed butterfly: after 5 stages lane l holds the warp sums of NACC*RG/32 entries
+  constexpr int TOT = NACC * RG;
+  double v[TOT];
+#pragma unroll
+  for (int a = 0; a < LINES; ++a)
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+#pragma unroll
+      for (int r = 0; r < RG; ++r) v[(a * W + k) * RG + r] = acc[a][k][r];
+  if constexpr (TOT % 32 == 0) {
+    int len = TOT;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool upper = (lane & s) != 0;
+      const int half = len / 2;
+#pragma unroll
+      for (int e = 0; e < TOT / 2; ++e) {
+        if (e < half) {
+          const double send = upper ? v[e] : v[e + half];
+          const double keep = upper ? v[e + half] : v[e];
+          v[e] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+      }
+      len = half;
+    }
+    // lane holds entries e' = lane-dependent block of size TOT/32
+    const int per = TOT / 32;
+    // the block index of this lane: bit s of lane selected the upper half at stage s
+    int blk = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) blk = blk * 2 + ((lane & s) ? 1 : 0);
+#pragma unroll
+    for (int e = 0; e < per; ++e) {
+      const int idx = blk * per + e;
+      const int r = idx % RG;
+      const int k = (idx / RG) % W;
+      const int ln = idx / (RG * W);
+      if (r < nr && v[e] != 0.0)
+        atomicAdd(g + r * rhs_stride + rowoff_dyn<D, MM>(ch.col, ln, n) + wrap_cell(top - MM + 1 + k, n), v[e]);
+    }
+  } else {
+    if (has) {
+#pragma unroll
+      for (int a = 0; a < LINES; ++a)
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+          for (int r = 0; r < RG; ++r)
+            if (r < nr && acc[a][k][r] != 0.0)
+              atomicAdd(g + r * rhs_stride + rowoff[a] + wrap_cell(top - MM + 1 + k, n), acc[a][k][r]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// gather: out[perm] += eta * interp
+// ----------------------------------------------------------------------------
+template <int D, int MM, int RG, int TAB>
+__global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const Window w, int n,
+                                                     const PolyTable T,
+                                                     const double* __restrict__ grid,
+                                                     int64_t rhs_stride, int nr,
+                                                     double* __restrict__ out, int64_t ldo) {
+  using C = SoloCfg<D, MM>;
+  constexpr int W = C::W, LINES = C::LINES;
+  const int lane = threadIdx.x & 31;
+  const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ci >= sv.nchunks) return;
+  const Chunk ch = sv.chunks[ci];
+  const double* g = grid + w.grid_off;
+  int64_t rowoff[LINES];
+#pragma unroll
+  for (int a = 0; a < LINES; ++a)
+    rowoff[a] = D == 2 ? (int64_t)wrap_cell(ch.col - MM + 1 + a, n) * n : 0;
+
+  double gv[LINES][W][RG];
+  auto load_slot = [&](int k, int c) {
+    const int cm = wrap_cell(c, n);
+#pragma unroll
+    for (int a = 0; a < LINES; ++a)
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        gv[a][k][r] = r < nr ? __ldg(g + r * rhs_stride + rowoff[a] + cm) : 0.0;
+  };
+  int cur = INT_MIN;
+  const int count = ch.count;
+  for (int q = lane; q < count; q += 32) {
+    const int64_t i = ch.begin + q;
+    double nx[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) nx[t] = __ldcs(sv.nx + t * sv.N + i);
+    const int j = __ldcs(sv.perm + i);
+    double prior[RG];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) prior[r] = r < nr ? out[r * ldo + j] : 0.0;
+    double wt[D][W];
+    int u;
+    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
+    if (u != cur) {
+      if (cur != INT_MIN && u - cur < W) {
+#pragma unroll 1
+        for (int c = cur; c < u; ++c) {
+#pragma unroll
+          for (int a = 0; a < LINES; ++a)
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+#pragma unroll
+              for (int k = 0; k + 1 < W; ++k) gv[a][k][r] = gv[a][k + 1][r];
+            }
+          load_slot(W - 1, c + MM + 1);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k) load_slot(k, u - MM + 1 + k);
+      }
+      cur = u;
+    }
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int ln = 0; ln < LINES; ++ln) {
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; k += 2) {
+          t0 = fma(wt[D - 1][k], gv[ln][k][r], t0);
+          if (k + 1 < W) t1 = fma(wt[D - 1][k + 1], gv[ln][k + 1][r], t1);
+        }
+        s = D == 2 ? fma(wt[0][ln], t0 + t1, s) : (t0 + t1);
+      }
+      if (r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, s));
+    }
+  }
+}
+
+}  // namespace afs
