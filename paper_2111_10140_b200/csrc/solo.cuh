@@ -70,6 +70,56 @@ struct SoloFits {
   static constexpr bool value = D <= 2 && SoloCfg<D, MM>::NACC * RG <= 64;
 };
 
+// Two-deep prefetch of a lane's node stream q, q+32, q+64 ...: stage 2 holds nx/perm of
+// q+64, stage 1 holds nx of q+32 and its gathered value val[perm] (alpha in the spread,
+// out in the gather), so the dependent random load has a full node of work to land.
+template <int D, int RG>
+struct SoloPipe {
+  double nx1[D], v1[RG], nx2[D];
+  int p1, p2;
+
+  __device__ __forceinline__ void load_node(const SortedSide& sv, const Chunk& ch, int q,
+                                            double (&nx)[D], int& p) {
+    if (q < ch.count) {
+      const int64_t i = ch.begin + q;
+#pragma unroll
+      for (int t = 0; t < D; ++t) nx[t] = __ldcs(sv.nx + t * sv.N + i);
+      p = __ldcs(sv.perm + i);
+    } else {
+#pragma unroll
+      for (int t = 0; t < D; ++t) nx[t] = 0.0;
+      p = -1;
+    }
+  }
+  __device__ __forceinline__ void load_val(const double* __restrict__ src, int64_t ld, int nr,
+                                           int p, double (&v)[RG]) {
+#pragma unroll
+    for (int r = 0; r < RG; ++r) v[r] = (p >= 0 && r < nr) ? src[r * ld + p] : 0.0;
+  }
+  __device__ __forceinline__ void prime(const SortedSide& sv, const Chunk& ch, int lane,
+                                        const double* __restrict__ src, int64_t ld, int nr) {
+    load_node(sv, ch, lane, nx1, p1);
+    load_val(src, ld, nr, p1, v1);
+    load_node(sv, ch, lane + 32, nx2, p2);
+  }
+  // returns node q's data (already in flight) and pushes q+64 into the pipe
+  __device__ __forceinline__ int advance(const SortedSide& sv, const Chunk& ch, int q,
+                                         double (&nx)[D], double (&v)[RG],
+                                         const double* __restrict__ src, int64_t ld, int nr) {
+    const int p = p1;
+#pragma unroll
+    for (int t = 0; t < D; ++t) nx[t] = nx1[t];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) v[r] = v1[r];
+#pragma unroll
+    for (int t = 0; t < D; ++t) nx1[t] = nx2[t];
+    p1 = p2;
+    load_val(src, ld, nr, p1, v1);
+    load_node(sv, ch, q + 64, nx2, p2);
+    return p;
+  }
+};
+
 __device__ __forceinline__ int warp_max_i(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -134,15 +184,13 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
 
   int cur = INT_MIN;
   const int count = ch.count;
+  // software pipeline: node data two steps ahead, alpha[perm] one step ahead
+  SoloPipe<D, RG> pipe;
+  pipe.prime(sv, ch, lane, alpha, lda, nr);
   for (int q = lane; q < count; q += 32) {
-    const int64_t i = ch.begin + q;
     double nx[D];
-#pragma unroll
-    for (int t = 0; t < D; ++t) nx[t] = __ldcs(sv.nx + t * sv.N + i);
-    const int j = __ldcs(sv.perm + i);
     double a[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) a[r] = r < nr ? __ldg(alpha + r * lda + j) : 0.0;
+    pipe.advance(sv, ch, q, nx, a, alpha, lda, nr);
     double wt[D][W];
     int u;
     solo_weights<D, MM, TAB>(nx, T, wt, u, n);
@@ -249,15 +297,12 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
   };
   int cur = INT_MIN;
   const int count = ch.count;
+  SoloPipe<D, RG> pipe;
+  pipe.prime(sv, ch, lane, out, ldo, nr);
   for (int q = lane; q < count; q += 32) {
-    const int64_t i = ch.begin + q;
     double nx[D];
-#pragma unroll
-    for (int t = 0; t < D; ++t) nx[t] = __ldcs(sv.nx + t * sv.N + i);
-    const int j = __ldcs(sv.perm + i);
-    double prior[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) prior[r] = r < nr ? out[r * ldo + j] : 0.0;
+    double prior[RG];   // out[perm] before this window (each node is written once)
+    const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
     double wt[D][W];
     int u;
     solo_weights<D, MM, TAB>(nx, T, wt, u, n);
