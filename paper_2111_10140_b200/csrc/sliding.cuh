@@ -135,20 +135,56 @@ struct NodesPerLane {
   static constexpr int P = D == 3 ? 1 : (D == 2 ? 2 : 4);
 };
 
-// one staging round: lane tl stages nodes tl + TEAM*p (p < P) of the batch at b0
-template <int D, int MM, int EXTRA, int TAB>
+// Staging-round input pipeline: lane tl stages nodes b0 + tl + TEAM*p (p < P).  Two rounds
+// in flight: stage 2 holds nx/perm of round b0+2*BATCH, stage 1 holds round b0+BATCH plus
+// its gathered value val[perm] (alpha in the spread, out in the gather), so the dependent
+// random load overlaps a whole round of work.
+template <int D, int MM, int EXTRA, int TAB, int RG>
 struct Round {
   using S = Stage<D, MM, EXTRA>;
-  static constexpr int P = S::P, TEAM = Cfg<D, MM>::TEAM;
-  NodeIn<D> nxt[P];
+  static constexpr int P = S::P, TEAM = Cfg<D, MM>::TEAM, BATCH = S::BATCH;
+  NodeIn<D> n1[P], n2[P];
+  double v1[P][RG];
 
-  __device__ __forceinline__ void prefetch(const SortedSide& sv, const Chunk& ch, bool active,
-                                           int tl, int b0) {
+  __device__ __forceinline__ void load_round(const SortedSide& sv, const Chunk& ch, bool active,
+                                             int tl, int b0, NodeIn<D> (&dst)[P]) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int q = b0 + tl + TEAM * p;
-      if (active && q < ch.count) load_node<D>(sv, ch.begin + q, nxt[p]);
+      if (active && q < ch.count) {
+        load_node<D>(sv, ch.begin + q, dst[p]);
+      } else {
+        dst[p].perm = -1;
+      }
     }
+  }
+  __device__ __forceinline__ void load_vals(const double* __restrict__ src, int64_t ld, int nr) {
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        v1[p][r] = (n1[p].perm >= 0 && r < nr) ? src[r * ld + n1[p].perm] : 0.0;
+  }
+  __device__ __forceinline__ void prime(const SortedSide& sv, const Chunk& ch, bool active, int tl,
+                                        const double* __restrict__ src, int64_t ld, int nr) {
+    load_round(sv, ch, active, tl, 0, n1);
+    load_vals(src, ld, nr);
+    load_round(sv, ch, active, tl, BATCH, n2);
+  }
+  // hand out round b0 (in flight since two rounds) and refill the pipe with b0 + 2*BATCH
+  __device__ __forceinline__ void advance(const SortedSide& sv, const Chunk& ch, bool active,
+                                          int tl, int b0, NodeIn<D> (&in)[P],
+                                          double (&val)[P][RG], const double* __restrict__ src,
+                                          int64_t ld, int nr) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      in[p] = n1[p];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) val[p][r] = v1[p][r];
+      n1[p] = n2[p];
+    }
+    load_vals(src, ld, nr);
+    load_round(sv, ch, active, tl, b0 + 2 * BATCH, n2);
   }
 };
 
@@ -291,24 +327,20 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
   int cur = INT_MIN;
   const int rounds = warp_max(ch.count);
   constexpr int P = S::P, BATCH = S::BATCH;
-  Round<D, MM, 1 + RG, TAB> rd;
-  rd.prefetch(sv, ch, active, tl, 0);
+  Round<D, MM, 1 + RG, TAB, RG> rd;
+  rd.prime(sv, ch, active, tl, alpha, lda, nr);
   for (int b0 = 0; b0 < rounds; b0 += BATCH) {
     {
       NodeIn<D> in[P];
       bool live[P];
       double* rows[P];
       double a[P][RG];
+      rd.advance(sv, ch, active, tl, b0, in, a, alpha, lda, nr);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        in[p] = rd.nxt[p];
-        live[p] = active && b0 + tl + TEAM * p < ch.count;
+        live[p] = in[p].perm >= 0;
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
-#pragma unroll
-        for (int r = 0; r < RG; ++r)
-          a[p][r] = (live[p] && r < nr) ? __ldg(alpha + r * lda + in[p].perm) : 0.0;
       }
-      rd.prefetch(sv, ch, active, tl, b0 + BATCH);
       stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, T, rows);
 #pragma unroll
       for (int p = 0; p < P; ++p)
@@ -393,26 +425,22 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   };
 
   const int rounds = warp_max(ch.count);
-  Round<D, MM, 1, TAB> rd;
-  rd.prefetch(sv, ch, active, tl, 0);
+  Round<D, MM, 1, TAB, RG> rd;
+  rd.prime(sv, ch, active, tl, out, ldo, nr);
   for (int b0 = 0; b0 < rounds; b0 += BATCH) {
     int my_perm[P];
-    double prior[P][RG];   // out[perm] before this window, loaded early (random access)
+    double prior[P][RG];   // out[perm] before this window (each node written once), prefetched
     {
       NodeIn<D> in[P];
       bool live[P];
       double* rows[P];
+      rd.advance(sv, ch, active, tl, b0, in, prior, out, ldo, nr);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        in[p] = rd.nxt[p];
-        live[p] = active && b0 + tl + TEAM * p < ch.count;
+        live[p] = in[p].perm >= 0;
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
-        my_perm[p] = live[p] ? in[p].perm : -1;
-#pragma unroll
-        for (int r = 0; r < RG; ++r)
-          prior[p][r] = (live[p] && r < nr) ? out[r * ldo + in[p].perm] : 0.0;
+        my_perm[p] = in[p].perm;
       }
-      rd.prefetch(sv, ch, active, tl, b0 + BATCH);
       stage_nodes<D, MM, 1, TAB, P>(in, live, n, T, rows);
     }
     __syncwarp();
