@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     rowoff[a] = D == 2 ? (int64_t)wrap_cell(ch.col - MM + 1 + a, n) * n : 0;
 
   double gv[LINES][W][RG];
-  double ahead[LINES][RG];   // grid column of cell cur + MM + 1 (prefetched)
+  // grid column of cell cur + MM + 1, prefetched when registers allow (2-D windows are at
+  // the 255-register limit already and rarely move their window)
+  constexpr bool PREFETCH = C::NACC * RG <= 16;
+  double ahead[LINES][RG];
   auto load_slot = [&](int k, int c) {
     const int cm = wrap_cell(c, n);
 #pragma unroll
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     int u;
     solo_weights<D, MM, TAB>(nx, T, wt, u, n);
     if (u != cur) {
-      if (u == cur + 1) {
+      if (PREFETCH && u == cur + 1) {
         // one-cell move: the entering cell was prefetched into `ahead`
 #pragma unroll
         for (int a = 0; a < LINES; ++a)
@@ -335,12 +338,14 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
         for (int k = 0; k < W; ++k) load_slot(k, u - MM + 1 + k);
       }
       cur = u;
-      const int cm = wrap_cell(u + MM + 1, n);
+      if (PREFETCH) {
+        const int cm = wrap_cell(u + MM + 1, n);
 #pragma unroll
-      for (int a = 0; a < LINES; ++a)
+        for (int a = 0; a < LINES; ++a)
 #pragma unroll
-        for (int r = 0; r < RG; ++r)
-          ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + rowoff[a] + cm) : 0.0;
+          for (int r = 0; r < RG; ++r)
+            ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + rowoff[a] + cm) : 0.0;
+      }
     }
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
