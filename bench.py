@@ -80,14 +80,9 @@ def algorithmic_bytes(N, windows, n, R=1):
 
 def lpt_assign(windows, N, m, world):
     """Longest-processing-time deal of windows to ranks on cost N*(2m)^d."""
-    order = sorted(range(len(windows)), key=lambda i: -(2 * m) ** len(windows[i]))
-    load = [0] * world
-    owner = [0] * len(windows)
-    for i in order:
-        r = min(range(world), key=lambda k: load[k])
-        owner[i] = r
-        load[r] += N * (2 * m) ** len(windows[i])
-    return owner
+    from paper_2111_10140_b200.distributed import lpt_assign as lpt, window_costs
+
+    return lpt(window_costs(windows, N, m), world)
 
 
 class ClockSampler:

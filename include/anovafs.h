@@ -112,6 +112,20 @@ int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info);
 int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out,
               int64_t ld_out, int32_t nrhs, void* stream);
 
+/* The three stages of afs_apply, for point-sharded multi-GPU use:
+ * afs_spread writes every window's oversampled grid (afs_plan_grids: base pointer,
+ * doubles per rhs = sum over windows of n^d_l, rhs r at grids + r*stride), the caller
+ * may all-reduce the grids across ranks, afs_spectral applies the multipliers in place,
+ * afs_gather interpolates into out (same conventions as afs_apply). */
+int afs_spread(afs_plan* plan, const double* alpha, int64_t ld_alpha, int32_t nrhs,
+               void* stream);
+int afs_spectral(afs_plan* plan, int32_t nrhs, void* stream);
+int afs_gather(afs_plan* plan, double* out, int64_t ld_out, int32_t nrhs, void* stream);
+int afs_plan_grids(afs_plan* plan, double** grids, int64_t* doubles_per_rhs);
+/* Let the caller own the grid buffer (e.g. a tensor registered with NCCL): capacity must be
+ * >= doubles_per_rhs * max_rhs; the plan stops using (and frees) its own buffer. */
+int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles);
+
 /* Stage profiling: when enabled, every afs_apply records CUDA events around
  * its spread / spectral / gather stages on the caller's stream, waits for them
  * and accumulates the device milliseconds (this adds one stream sync per

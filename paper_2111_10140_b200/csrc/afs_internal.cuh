@@ -72,6 +72,7 @@ struct afs_plan {
   double* mult = nullptr;           // all multipliers
   double2* twiddle = nullptr;       // n entries e^{-2 pi i k / n}
   double* grids = nullptr;          // [rhs][sum of cells]  (rhs-major)
+  bool grids_owned = true;          // false after afs_plan_bind_grids
   int64_t grid_total = 0;           // sum of cells over windows
   double2* scratch_a = nullptr;
   double2* scratch_b = nullptr;

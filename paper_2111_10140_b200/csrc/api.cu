@@ -80,7 +80,7 @@ static void free_plan(afs_plan* p) {
   cudaFree(p->tgt);
   cudaFree(p->mult);
   cudaFree(p->twiddle);
-  cudaFree(p->grids);
+  if (p->grids_owned) cudaFree(p->grids);
   cudaFree(p->scratch_a);
   cudaFree(p->scratch_b);
   cudaFree(p->cg.r);
@@ -250,6 +250,61 @@ int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info) {
     info->n_sources = plan->Ns;
     info->n_targets = plan->Nt;
     info->kernel_launches_per_apply = plan->launches_per_apply;
+  });
+}
+
+static void check_rhs(const afs_plan* plan, int32_t nrhs) {
+  if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
+  if (nrhs < 1 || nrhs > plan->max_rhs) throw afs::Error(AFS_ERR_SHAPE, "nrhs must lie in 1..max_rhs");
+}
+
+int afs_spread(afs_plan* plan, const double* alpha, int64_t ld_alpha, int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    check_rhs(plan, nrhs);
+    if (!alpha || ld_alpha < plan->Ns) throw afs::Error(AFS_ERR_SHAPE, "bad alpha");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    afs::spread_all(plan, alpha, ld_alpha, nrhs, (cudaStream_t)stream);
+  });
+}
+
+int afs_spectral(afs_plan* plan, int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    check_rhs(plan, nrhs);
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    afs::spectral_all(plan, nrhs, (cudaStream_t)stream);
+  });
+}
+
+int afs_gather(afs_plan* plan, double* out, int64_t ld_out, int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    check_rhs(plan, nrhs);
+    if (!out || ld_out < plan->Nt) throw afs::Error(AFS_ERR_SHAPE, "bad out");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    afs::gather_all(plan, out, ld_out, nrhs, (cudaStream_t)stream);
+  });
+}
+
+int afs_plan_grids(afs_plan* plan, double** grids, int64_t* doubles_per_rhs) {
+  return afs::guarded([&] {
+    if (!plan || !grids || !doubles_per_rhs) throw afs::Error(AFS_ERR_VALIDATION, "null argument");
+    *grids = plan->grids;
+    *doubles_per_rhs = plan->grid_total;
+  });
+}
+
+int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles) {
+  return afs::guarded([&] {
+    if (!plan || !buffer) throw afs::Error(AFS_ERR_VALIDATION, "null plan/buffer");
+    if (capacity_doubles < plan->grid_total * plan->max_rhs)
+      throw afs::Error(AFS_ERR_SHAPE, "grid buffer smaller than doubles_per_rhs * max_rhs");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    if (plan->grids_owned) cudaFree(plan->grids);
+    plan->grids = buffer;
+    plan->grids_owned = false;
   });
 }
 

@@ -1,0 +1,178 @@
+"""Multi-GPU ANOVA matvec: one process per GPU, torch.distributed (NCCL) plumbing.
+
+The reference has no parallelism.  The path shards naturally
+in one exchange step per matvec:
+
+* ``WindowSharded`` (C3/C5: many windows) — windows are dealt to ranks by
+  LPT on their spread+gather cost ``N (2m)^d_l``; every rank holds all
+  points and alpha, computes ``sum_{l in S_rank} eta_l K_l alpha`` and one
+  all-reduce sums the N-vector partials.  The terms are independent
+  (anova.py:179-183), so the result equals the single-GPU sum up to the
+  order of the cross-window additions.
+* ``PointSharded`` (C4: one window, huge N) — every rank owns N/p points and
+  their alpha; the bbox (hence center/scale) is all-reduced first so every
+  rank builds the same multiplier; each rank spreads its points onto a full
+  grid, the grids are all-reduced (the spread is linear in the node set,
+  nfft.py:241-245), every rank runs the spectral stage and gathers its own
+  points.  The output stays row-sharded.
+
+Both classes take the local compute as injectable backends so the
+orchestration is testable on CPU (gloo) without a GPU (tests/test_distributed.py);
+the default backends are the CUDA operators of this package.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .params import AccuracyProfile, PeriodizationConfig
+
+
+def lpt_assign(costs, world):
+    """Longest-processing-time deal: returns owner rank per item (ties -> lowest rank)."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0.0] * world
+    owner = [0] * len(costs)
+    for i in order:
+        r = min(range(world), key=lambda k: (load[k], k))
+        owner[i] = r
+        load[r] += costs[i]
+    return owner
+
+
+def window_costs(windows, N, m):
+    """Spread+gather touch cost of each window, N (2m)^d_l."""
+    return [float(N) * (2 * m) ** len(w) for w in windows]
+
+
+class WindowSharded:
+    """Window-sharded ANOVA operator.
+
+    ``make_local(windows, weights)`` returns a callable ``alpha -> partial`` for
+    this rank's windows (default: a CUDA ``AnovaKernelOperator`` on device
+    tensors).  ``apply`` returns the full sum on every rank.
+    """
+
+    def __init__(self, X, windows, sigma, *, M=64, m=4, oversampling=2.0, group=None,
+                 make_local=None, device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.windows = [tuple(w) for w in windows]
+        P = len(self.windows)
+        self.N = X.shape[0]
+        self.owner = lpt_assign(window_costs(self.windows, self.N, m), self.world)
+        self.mine = [l for l in range(P) if self.owner[l] == self.rank]
+        weights = [1.0 / P] * len(self.mine)
+        if make_local is None:
+            make_local = _cuda_window_backend(X, sigma, M, m, oversampling, device)
+        self.local = make_local([self.windows[l] for l in self.mine], weights) if self.mine else None
+
+    def apply(self, alpha):
+        import torch
+
+        if self.local is not None:
+            part = self.local(alpha)
+        else:
+            part = torch.zeros_like(alpha)
+        part = part.contiguous()
+        self.dist.all_reduce(part, group=self.group)
+        return part
+
+
+def _cuda_window_backend(X, sigma, M, m, oversampling, device):
+    from .operators import AnovaKernelOperator
+
+    def make(windows, weights):
+        op = AnovaKernelOperator(X, windows, sigma, AccuracyProfile("sharded", oversampling, m), None,
+                                 PeriodizationConfig(coeff_grid=M), strict=False, weights=weights,
+                                 device=device)
+        return op.apply
+    return make
+
+
+def global_bbox(X_local, windows, group=None):
+    """Per-window (min, max) over all ranks' points (all-reduce MIN / MAX)."""
+    import torch
+    import torch.distributed as dist
+
+    out = []
+    for w in windows:
+        sub = X_local[:, list(w)]
+        if isinstance(sub, np.ndarray):
+            lo = torch.from_numpy(sub.min(axis=0).copy())
+            hi = torch.from_numpy(sub.max(axis=0).copy())
+        else:
+            lo, hi = sub.amin(dim=0).clone(), sub.amax(dim=0).clone()
+        dev = torch.device("cuda", torch.cuda.current_device()) if (
+            dist.get_backend(group) == "nccl") else torch.device("cpu")
+        lo, hi = lo.to(dev), hi.to(dev)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+        out.append((lo.cpu().numpy(), hi.cpu().numpy()))
+    return out
+
+
+class PointSharded:
+    """Point-sharded fast summation (one or more windows, all ranks share the grids).
+
+    ``backend`` must provide ``spread(alpha) -> grids`` (a tensor this class
+    all-reduces in place), ``spectral(grids)`` and ``gather(grids) -> out``.
+    """
+
+    def __init__(self, backend, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.backend = backend
+
+    def apply(self, alpha_local):
+        grids = self.backend.spread(alpha_local)
+        self.dist.all_reduce(grids, group=self.group)
+        self.backend.spectral(grids)
+        return self.backend.gather(grids)
+
+
+class CudaPointBackend:
+    """Stage backend over a CUDA plan whose grid buffer is a torch tensor (NCCL-visible)."""
+
+    def __init__(self, X_local, windows, sigma, *, M, m, oversampling=2.0, weights=None,
+                 max_rhs=1, group=None, device=None):
+        import torch
+
+        from .operators import AnovaKernelOperator, bbox_scaling
+
+        cfg = PeriodizationConfig(coeff_grid=M)
+        boxes = global_bbox(X_local, windows, group)
+        scaling = [bbox_scaling(lo, hi, cfg) for lo, hi in boxes]
+        P = len(windows)
+        self.op = AnovaKernelOperator(X_local, windows, sigma, AccuracyProfile("pts", oversampling, m),
+                                      None, cfg, strict=False,
+                                      weights=weights if weights is not None else [1.0 / P] * P,
+                                      device=device, max_rhs=max_rhs, scaling=scaling)
+        self.plan = self.op._plan
+        per = self.plan.grid_doubles_per_rhs()
+        self.grids = torch.zeros(per * self.plan.max_rhs, dtype=torch.float64,
+                                 device=self.plan.device)
+        self.plan.bind_grids(self.grids)
+        self.R = 1
+
+    def spread(self, alpha):
+        a = alpha if alpha.dim() == 2 else alpha[None, :]
+        self.R = a.shape[0]
+        self.plan.spread_device(a.contiguous(), self.R)
+        return self.grids[: self.plan.grid_doubles_per_rhs() * self.R]
+
+    def spectral(self, grids):
+        self.plan.spectral_device(self.R)
+
+    def gather(self, grids):
+        import torch
+
+        out = torch.empty((self.R, self.plan.Nt), dtype=torch.float64, device=self.plan.device)
+        self.plan.gather_device(out, self.R)
+        return out

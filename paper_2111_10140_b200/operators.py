@@ -111,6 +111,21 @@ class WindowOperator:
         self.n_targets = n_targets
 
 
+def bbox_scaling(lo, hi, config):
+    """(center, scale) from per-column min/max (fastsum.py:210-217, same arithmetic)."""
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    diameter = float(np.linalg.norm(hi - lo))                       # fastsum.py:213
+    scale = config.ball_radius / diameter if diameter > 0 else 1.0  # fastsum.py:216
+    center = (lo + hi) / 2.0                                        # fastsum.py:217
+    return center, scale
+
+
+def _chunks(n, size=1 << 20):
+    """[lo, hi) ranges of ~8 MB (fp64) for pipelined host<->device copies."""
+    return [(lo, min(n, lo + size)) for lo in range(0, n, size)]
+
+
 def _columns_minmax(A, cols):
     """(mins, maxs) of the selected columns, computed where A lives."""
     if isinstance(A, np.ndarray):
@@ -145,7 +160,7 @@ class _Plan:
     """Owns one native plan (afs_plan*) and its staging buffers."""
 
     def __init__(self, X, Z, feats, weights, kernel, config, profile, device, max_rhs,
-                 window_eval="poly"):
+                 window_eval="poly", scaling=None):
         torch = _torch()
         self.lib = _native.load()
         self.device = torch.device("cuda", device if device is not None else torch.cuda.current_device())
@@ -163,13 +178,15 @@ class _Plan:
         descs = (_native.WindowDesc * len(feats))()
         self._keep = []
         for l, (w, eta) in enumerate(zip(feats, weights)):
-            lo, hi = _columns_minmax(X, w)
-            if Z is not None:
-                zlo, zhi = _columns_minmax(Z, w)
-                lo, hi = np.minimum(lo, zlo), np.maximum(hi, zhi)
-            diameter = float(np.linalg.norm(hi - lo))                       # fastsum.py:213
-            scale = config.ball_radius / diameter if diameter > 0 else 1.0  # fastsum.py:216
-            center = (lo + hi) / 2.0                                        # fastsum.py:217
+            if scaling is not None:
+                # externally fixed (e.g. bbox all-reduced over point shards)
+                center, scale = np.asarray(scaling[l][0], dtype=np.float64), float(scaling[l][1])
+            else:
+                lo, hi = _columns_minmax(X, w)
+                if Z is not None:
+                    zlo, zhi = _columns_minmax(Z, w)
+                    lo, hi = np.minimum(lo, zlo), np.maximum(hi, zhi)
+                center, scale = bbox_scaling(lo, hi, config)
             coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w))
             mult = window_multiplier(coeffs, M, n, m)
             self._keep.append(mult)
@@ -247,6 +264,33 @@ class _Plan:
         _native.check(self.lib.afs_apply(self.handle, alpha.data_ptr(), self.N, out.data_ptr(),
                                          self.Nt, int(nrhs), stream))
 
+    # -- stage-level entry points (point-sharded multi-GPU) ---------------------------
+    def grid_doubles_per_rhs(self):
+        ptr = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _native.check(self.lib.afs_plan_grids(self.handle, ctypes.byref(ptr), ctypes.byref(n)))
+        return int(n.value)
+
+    def bind_grids(self, buf):
+        """Make the plan spread into / read from `buf` (cuda float64, >= per_rhs*max_rhs)."""
+        _native.check(self.lib.afs_plan_bind_grids(self.handle, buf.data_ptr(), buf.numel()))
+        self._bound_grids = buf   # keep alive
+
+    def spread_device(self, alpha, nrhs):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.afs_spread(self.handle, alpha.data_ptr(), self.N, int(nrhs), stream))
+
+    def spectral_device(self, nrhs):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.afs_spectral(self.handle, int(nrhs), stream))
+
+    def gather_device(self, out, nrhs):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.afs_gather(self.handle, out.data_ptr(), self.Nt, int(nrhs), stream))
+
     def cg_device(self, b, x, beta, tol, maxiter):
         torch = _torch()
         stream = torch.cuda.current_stream(self.device).cuda_stream
@@ -295,13 +339,26 @@ class _Plan:
                       torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=True))
                 self._stage[R] = st
             h_in, d_in, d_out, h_out = st
-            h_in.numpy()[...] = arr[None, :] if one else arr.T
-            d_in.copy_(h_in, non_blocking=True)
+            stream = torch.cuda.current_stream(self.device)
+            src = torch.from_numpy(np.ascontiguousarray(arr.T) if not one else arr)
+            src = src[None, :] if one else src
+            # chunked host->pinned (multi-threaded torch copy) overlapped with async H2D
+            for lo, hi in _chunks(self.N):
+                h_in[:, lo:hi].copy_(src[:, lo:hi])
+                d_in[:, lo:hi].copy_(h_in[:, lo:hi], non_blocking=True)
             self.apply_device(d_in, d_out, R)
-            h_out.copy_(d_out, non_blocking=True)
-            torch.cuda.current_stream(self.device).synchronize()
-            res = h_out.numpy()
-            return res[0].copy() if one else res.T.copy()
+            res = np.empty((R, self.Nt))
+            dst = torch.from_numpy(res)
+            events = []
+            for lo, hi in _chunks(self.Nt):
+                h_out[:, lo:hi].copy_(d_out[:, lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                events.append((lo, hi, ev))
+            for lo, hi, ev in events:   # pinned->host copy of chunk k overlaps D2H of k+1..
+                ev.synchronize()
+                dst[:, lo:hi].copy_(h_out[:, lo:hi])
+            return res[0] if one else res.T
 
 
 class AnovaKernelOperator:
@@ -314,7 +371,8 @@ class AnovaKernelOperator:
     """
 
     def __init__(self, X, windows, sigma, profile="default", targets=None, config=None, *,
-                 strict=True, weights=None, device=None, max_rhs=1, window_eval="poly"):
+                 strict=True, weights=None, device=None, max_rhs=1, window_eval="poly",
+                 scaling=None):
         X = _as_matrix(X, "sources")
         if strict:
             if not isinstance(windows, WindowSet):
@@ -343,7 +401,7 @@ class AnovaKernelOperator:
         self.n_sources = X.shape[0]
         self.n_targets = X.shape[0] if Z is None else Z.shape[0]
         self._plan = _Plan(X, Z, list(windows.windows), list(windows.weights), kernel, config,
-                           profile, device, max_rhs, window_eval)
+                           profile, device, max_rhs, window_eval, scaling)
         self.operators = self._plan.windows
 
     def apply(self, alpha):

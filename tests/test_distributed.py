@@ -1,0 +1,183 @@
+"""Multi-rank orchestration on CPU (gloo, world_size 2): window sharding and point
+sharding must reproduce the single-process ANOVA sum.  The local compute is the
+CPU oracle / a numpy model of the device stages (test infrastructure); the
+CUDA backends of the same classes run on the GPU box."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
+
+from paper_2111_10140_b200.distributed import lpt_assign, window_costs  # noqa: E402
+from paper_2111_10140_b200 import synthetic  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(fn, world, *args):
+    port = _free_port()
+    mp.spawn(fn, args=(world, port) + args, nprocs=world, join=True)
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def test_lpt_balances_c3_windows():
+    w = synthetic.C3_WINDOWS
+    costs = window_costs(w, 10_000_000, 4)
+    for world in (1, 2, 4, 8):
+        owner = lpt_assign(costs, world)
+        loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
+        assert sorted(set(owner)) == list(range(world))
+        # LPT bound: max load <= 4/3 optimum (and >= the mean)
+        assert max(loads) <= 4.0 / 3.0 * max(sum(costs) / world, max(costs)) + 1e-6
+        assert owner == lpt_assign(costs, world)   # deterministic
+
+
+# --------------------------------------------------------------------------- window sharding
+def _window_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    from oracle import fastsum_oracle as orc
+    from paper_2111_10140_b200.distributed import WindowSharded
+
+    w = synthetic.c3(N=400)
+
+    def make_local(windows, weights):
+        def apply(alpha):
+            a = alpha.numpy()
+            s = np.zeros(w.N)
+            for eta, win in zip(weights, windows):
+                s += eta * orc.fastsum_apply(w.X[:, list(win)], a, w.sigma, w.M, w.m)
+            return torch.from_numpy(s)
+        return apply
+
+    op = WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, make_local=make_local)
+    res = op.apply(torch.from_numpy(w.alpha.copy())).numpy()
+    np.save(out_path + f".{rank}.npy", res)
+    dist.destroy_process_group()
+
+
+def test_window_sharded_matches_single_process(tmp_path):
+    from oracle import fastsum_oracle as orc
+
+    out = str(tmp_path / "ws")
+    _run(_window_worker, 2, out)
+    w = synthetic.c3(N=400)
+    ref = orc.anova_apply(w.X, w.windows, w.alpha, w.sigma, w.M, w.m)
+    for r in range(2):
+        got = np.load(out + f".{r}.npy")
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-13
+
+
+# --------------------------------------------------------------------------- point sharding
+class NumpyPointBackend:
+    """numpy model of the device stages for one window (spread / spectral / gather)."""
+
+    def __init__(self, X_local, win, sigma, M, m, group=None):
+        from oracle import fastsum_oracle as orc
+        from paper_2111_10140_b200 import GaussianKernel, PeriodizationConfig, regularize_kernel
+        from paper_2111_10140_b200.distributed import global_bbox
+        from paper_2111_10140_b200.operators import bbox_scaling
+        from paper_2111_10140_b200.spectrum import window_multiplier
+
+        self.orc = orc
+        cfg = PeriodizationConfig(coeff_grid=M)
+        (lo, hi), = global_bbox(X_local, [win], group)
+        center, scale = bbox_scaling(lo, hi, cfg)
+        self.d = len(win)
+        self.n = 2 * M
+        self.M, self.m = M, m
+        self.b = np.pi * (2.0 - M / self.n)
+        self.E = window_multiplier(regularize_kernel(GaussianKernel(sigma * scale), cfg, self.d),
+                                   M, self.n, m)
+        self.xs = (X_local[:, list(win)] - center) * scale
+
+    def _tensor(self):
+        n, m = self.n, self.m
+        flat, w = None, None
+        for t in range(self.d):
+            nx = n * self.xs[:, t]
+            c = np.floor(nx)[:, None] + np.arange(1 - m, m + 1)[None, :]
+            idx = np.mod(c, n).astype(np.int64)
+            val = self.orc.kb_window(nx[:, None] - c, m, self.b)
+            if flat is None:
+                flat, w = idx, val
+            else:
+                flat = (flat[:, :, None] * n + idx[:, None, :]).reshape(len(nx), -1)
+                w = (w[:, :, None] * val[:, None, :]).reshape(len(nx), -1)
+        return flat, w
+
+    def spread(self, alpha):
+        flat, w = self._tensor()
+        g = np.bincount(flat.ravel(), (alpha.numpy()[:, None] * w).ravel(), minlength=self.n ** self.d)
+        self.grids = torch.from_numpy(g)
+        return self.grids
+
+    def spectral(self, grids):
+        n, M, d = self.n, self.M, self.d
+        H = M // 2 + 1
+        g = grids.numpy().reshape((n,) * d)
+        sym = (np.arange(M + 1) - M // 2) % n
+        A = np.fft.fft(g, axis=-1)[..., :H]
+        if d == 3:
+            A = np.fft.fft(A, axis=1)[:, sym, :]
+        if d >= 2:
+            F = np.fft.fft(A, axis=0)
+            Y = np.zeros_like(F)
+            Y[sym] = F[sym] * self.E
+            A = n * np.fft.ifft(Y, axis=0)
+        else:
+            A = A * self.E
+        if d == 3:
+            full = np.zeros((n, n, H), dtype=complex)
+            full[:, sym, :] = A
+            A = n * np.fft.ifft(full, axis=1)
+        line = np.zeros(A.shape[:-1] + (n,), dtype=complex)
+        line[..., :H] = A
+        grids.copy_(torch.from_numpy((n * np.fft.ifft(line, axis=-1)).real.ravel()))
+
+    def gather(self, grids):
+        flat, w = self._tensor()
+        return torch.from_numpy((grids.numpy()[flat] * w).sum(1))
+
+
+def _point_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    from paper_2111_10140_b200.distributed import PointSharded
+
+    wl = synthetic.c4(N=600, R=1)
+    shard = np.array_split(np.arange(wl.N), world)[rank]
+    be = NumpyPointBackend(wl.X[shard], (0, 1, 2), wl.sigma, wl.M, wl.m)
+    res = PointSharded(be).apply(torch.from_numpy(wl.alpha[shard, 0].copy())).numpy()
+    np.save(out_path + f".{rank}.npy", res)
+    dist.destroy_process_group()
+
+
+def test_point_sharded_matches_single_process(tmp_path):
+    from oracle import fastsum_oracle as orc
+
+    out = str(tmp_path / "ps")
+    _run(_point_worker, 2, out)
+    wl = synthetic.c4(N=600, R=1)
+    ref = orc.fastsum_apply(wl.X, wl.alpha[:, 0], wl.sigma, wl.M, wl.m)
+    got = np.concatenate([np.load(out + f".{r}.npy") for r in range(2)])
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
