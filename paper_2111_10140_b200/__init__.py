@@ -3,7 +3,8 @@
 Drop-in for the reference's operator API on the hot path:
 ``FastsumOperator`` / ``AnovaKernelOperator`` ``.apply`` and ``cg_solve``,
 running hand-written sm_100a CUDA kernels behind the C ABI in
-``include/anovafs.h`` (``libanovafs.so``).
+``include/anovafs.h`` (``libanovafs.so``); plus the KRR wrappers that call it
+(``fit`` / ``decision_values`` / ``predict`` / model IO).
 """
 
 __version__ = "0.1.0"
@@ -14,12 +15,16 @@ from .params import (PROFILES, AccuracyProfile, GaussianKernel, GridSpec, Period
 from .spectrum import regularize_kernel
 from .operators import (AnovaKernelOperator, FastsumOperator, FreeWindowSet, WindowSet,
                         anova_apply, anova_build, fastsum_apply, fastsum_build)
-from .krr import CgResult, KernelSystem, cg_solve
+from .krr import (CgResult, KernelSystem, KrrConfig, KrrModel, cg_solve, decision_values, fit,
+                  load_model, model_from_dict, model_to_dict, predict, save_model)
+from .windowing import MisReport, ScalerStats, build_windows, mis_scores, zscore_apply, zscore_fit
 
 __all__ = [
     "AccuracyProfile", "AnovaKernelOperator", "CgResult", "DeviceError", "FastsumOperator",
-    "FreeWindowSet", "GaussianKernel", "GridSpec", "KernelSystem", "NumericalError", "PROFILES",
-    "PeriodizationConfig", "ShapeError", "ValidationError", "WindowSet", "anova_apply",
-    "anova_build", "cg_solve", "fastsum_apply", "fastsum_build", "regularize_kernel",
-    "resolve_profile",
+    "FreeWindowSet", "GaussianKernel", "GridSpec", "KernelSystem", "KrrConfig", "KrrModel",
+    "MisReport", "NumericalError", "PROFILES", "PeriodizationConfig", "ScalerStats", "ShapeError",
+    "ValidationError", "WindowSet", "anova_apply", "anova_build", "build_windows", "cg_solve",
+    "decision_values", "fastsum_apply", "fastsum_build", "fit", "load_model", "mis_scores",
+    "model_from_dict", "model_to_dict", "predict", "regularize_kernel", "resolve_profile",
+    "save_model", "zscore_apply", "zscore_fit",
 ]
