@@ -22,3 +22,11 @@ def fastsum_inputs(tag, d, N, n_tgt):
     Z = rng.normal(size=(n_tgt, d)) if n_tgt else None
     alpha = rng.standard_normal(N)
     return X, Z, alpha
+
+
+def krr_inputs(seed=31, n=700, n_test=300, d=7):
+    rng = np.random.default_rng(seed)
+    X = rng.normal(size=(n + n_test, d)) * rng.uniform(0.5, 3.0, size=d) + rng.normal(size=d)
+    w = rng.normal(size=d)
+    y = np.where(np.sin(X) @ w + 0.2 * rng.normal(size=n + n_test) >= 0, 1, -1)
+    return X[:n], y[:n], X[n:], y[n:]

@@ -13,13 +13,10 @@ import nfftkrr  # noqa: E402  (the reference)
 from nfftkrr import KrrConfig, decision_values, fit, mis_scores, predict  # noqa: E402
 from nfftkrr.krr import model_to_dict  # noqa: E402
 
+sys.path.insert(0, HERE)
+from cases import krr_inputs  # noqa: E402
 
-def krr_inputs(seed=31, n=700, n_test=300, d=7):
-    rng = np.random.default_rng(seed)
-    X = rng.normal(size=(n + n_test, d)) * rng.uniform(0.5, 3.0, size=d) + rng.normal(size=d)
-    w = rng.normal(size=d)
-    y = np.where(np.sin(X) @ w + 0.2 * rng.normal(size=n + n_test) >= 0, 1, -1)
-    return X[:n], y[:n], X[n:], y[n:]
+
 
 
 def main():

@@ -10,7 +10,7 @@ import pytest
 from conftest import rel_l2
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
-from make_golden_krr import krr_inputs  # noqa: E402
+from cases import krr_inputs  # noqa: E402
 
 import paper_2111_10140_b200 as afs  # noqa: E402
 
