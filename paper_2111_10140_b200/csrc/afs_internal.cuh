@@ -39,10 +39,20 @@ struct Window {
   int64_t grid_off;    // offset of this window's grid block (per rhs: cells)
   int64_t mult_len;    // (M+1)^(d-1) * (M/2+1)
   int64_t mult_off;    // offset into plan->mult
+  int64_t scratch_a_off, scratch_b_off;   // per-window spectral scratch (double2, x max_rhs)
 };
 
 struct SortedSide;   // geometry.cuh
 struct PolyTable;    // geometry.cuh
+
+struct GraphEntry {
+  const double* alpha;
+  int64_t lda;
+  double* out;
+  int64_t ldo;
+  int R;
+  cudaGraphExec_t exec;
+};
 
 struct CgScratch {
   double* r = nullptr;
@@ -85,6 +95,10 @@ struct afs_plan {
   int kb_tab = 0;                      // compile-time KB table id (kb_table_id)
   std::vector<afs::SortedSide*> src_side, tgt_side;
   afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
+  bool use_graphs = true;
+  std::vector<afs::GraphEntry> graphs;
+  cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};

@@ -46,12 +46,68 @@ void make_twiddles(afs_plan* p) {
   p->device_bytes += sizeof(double2) * p->n;
 }
 
+static void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                         int R, cudaStream_t s) {
+  spread_all(p, alpha, lda, R, s);
+  spectral_all(p, R, s);
+  gather_all(p, out, ldo, R, s);
+}
+
+// The ~2P + 4P launches of one apply are replayed from a CUDA graph keyed by the call's
+// pointers/shape.  A key is captured on its second use (the first, eager call performs any
+// one-time cudaFuncSetAttribute), so CG iterations and benchmark loops run graph launches.
+static bool apply_graph(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                        int R, cudaStream_t s) {
+  if (!p->use_graphs || s == nullptr) return false;   // legacy stream cannot be captured
+  GraphEntry* hit = nullptr;
+  for (GraphEntry& g : p->graphs)
+    if (g.alpha == alpha && g.lda == lda && g.out == out && g.ldo == ldo && g.R == R) hit = &g;
+  if (hit && hit->exec) {
+    AFS_CUDA(cudaGraphLaunch(hit->exec, s));
+    return true;
+  }
+  if (!hit) {
+    if (p->graphs.size() >= 8) {
+      if (p->graphs.front().exec) cudaGraphExecDestroy(p->graphs.front().exec);
+      p->graphs.erase(p->graphs.begin());
+    }
+    p->graphs.push_back(GraphEntry{alpha, lda, out, ldo, R, nullptr});
+    return false;   // first use: eager
+  }
+  cudaGraph_t graph = nullptr;
+  AFS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    apply_stages(p, alpha, lda, out, ldo, R, s);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  AFS_CUDA(cudaStreamEndCapture(s, &graph));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  AFS_CUDA(e);
+  hit->exec = exec;
+  AFS_CUDA(cudaGraphLaunch(exec, s));
+  return true;
+}
+
 void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo, int R,
                 cudaStream_t s) {
   if (!p->profiling) {
-    spread_all(p, alpha, lda, R, s);
-    spectral_all(p, R, s);
-    gather_all(p, out, ldo, R, s);
+    // run on the plan's own (capturable) stream, ordered after / before the caller's stream
+    if (!p->istream) {
+      AFS_CUDA(cudaStreamCreateWithFlags(&p->istream, cudaStreamNonBlocking));
+      AFS_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+      AFS_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+    }
+    AFS_CUDA(cudaEventRecord(p->ev_in, s));
+    AFS_CUDA(cudaStreamWaitEvent(p->istream, p->ev_in, 0));
+    if (!apply_graph(p, alpha, lda, out, ldo, R, p->istream))
+      apply_stages(p, alpha, lda, out, ldo, R, p->istream);
+    AFS_CUDA(cudaEventRecord(p->ev_out, p->istream));
+    AFS_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
     return;
   }
   for (int i = 0; i < 4; ++i)
@@ -90,6 +146,11 @@ static void free_plan(afs_plan* p) {
   cudaFree(p->cg.scalars);
   for (int i = 0; i < 4; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  for (afs::GraphEntry& g : p->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (p->istream) cudaStreamDestroy(p->istream);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
   for (SortedSide* s : p->src_side)
     if (s) { free_sorted_side(s); delete s; }
@@ -160,10 +221,13 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       for (int t = 1; t < w.d; ++t) w.mult_len *= K;
       w.mult_off = mult_total;
       mult_total += w.mult_len;
-      if (w.d == 2) a_len = std::max<int64_t>(a_len, (int64_t)p->n * p->H);
+      // per-window spectral scratch so that windows of one dimension run in one launch
+      w.scratch_a_off = a_len * d->max_rhs;
+      w.scratch_b_off = b_len * d->max_rhs;
+      if (w.d == 2) a_len += (int64_t)p->n * p->H;
       if (w.d == 3) {
-        a_len = std::max<int64_t>(a_len, (int64_t)p->n * p->n * p->H);
-        b_len = std::max<int64_t>(b_len, (int64_t)p->n * K * p->H);
+        a_len += (int64_t)p->n * p->n * p->H;
+        b_len += (int64_t)p->n * K * p->H;
       }
       launches += 1 + (w.d == 1 ? 1 : (w.d == 2 ? 3 : 5));
     }
@@ -305,6 +369,9 @@ int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles
     if (plan->grids_owned) cudaFree(plan->grids);
     plan->grids = buffer;
     plan->grids_owned = false;
+    for (afs::GraphEntry& g : plan->graphs)   // captured graphs reference the old buffer
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    plan->graphs.clear();
   });
 }
 
