@@ -149,15 +149,11 @@ class NodeGeometry:
 
 def gaussian_derivative(order: int, r: float, sigma: float) -> float:
     """fastsum.py:39-46: d^j/dr^j exp(-(r/sigma)^2) via physicists' Hermite H_j."""
-    t = r / sigma
-    # three-term recurrence H_{j+1} = 2t H_j - 2j H_{j-1}
-    h_prev, h = 1.0, 2.0 * t
-    if order == 0:
-        h = 1.0
-    else:
-        for j in range(1, order):
-            h_prev, h = h, 2.0 * t * h - 2.0 * j * h_prev
-    return (-1.0 / sigma) ** order * h * math.exp(-t * t)
+    t = np.float64(r) / sigma
+    # numpy's Clenshaw evaluation of H_order, as the reference does (bit-identical c_hat)
+    sel = np.zeros(order + 1)
+    sel[order] = 1.0
+    return (-1.0 / sigma) ** order * np.polynomial.hermite.hermval(t, sel) * np.exp(-t * t)
 
 
 def blend_coefficients(sigma: float, L: float = BALL_RADIUS, ell: float = TRANSITION_WIDTH,

@@ -21,7 +21,7 @@ from cases import krr_inputs  # noqa: E402
 
 def main():
     X, y, Xt, yt = krr_inputs()
-    cfg = KrrConfig(sigma=1.5, lam=0.5, cg_tol=1e-8, cg_maxiter=300)
+    cfg = KrrConfig(sigma=1.5, lam=0.5, cg_tol=1e-10, cg_maxiter=300)
     model = fit(X, y, cfg)
     doc = model_to_dict(model)
     g = {
