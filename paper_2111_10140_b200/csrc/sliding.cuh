@@ -193,7 +193,7 @@ struct Round {
 // the mirrored stencil position.
 template <int D, int MM, int EXTRA, int TAB, int P>
 __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool (&live)[P], int n,
-                                            const PolyTable& T, double* const (&row)[P]) {
+                                            const KbSmem<MM>& ks, double* const (&row)[P]) {
   constexpr int W = 2 * MM;
   double x[P][D];
   int pos0[P][D];   // store position of offset 0; step +1 or -1 (mirrored)
@@ -223,13 +223,18 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
+    for (int ip = 0; ip < MM; ++ip) {
+      const double2 c2 = lds_volatile2(&ks.c[k][ip]);
 #pragma unroll
-      for (int p = 0; p < P; ++p)
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * ip + h;
+        const double c = h ? c2.y : c2.x;
 #pragma unroll
-        for (int t = 0; t < D; ++t)
-          v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
+        for (int p = 0; p < P; ++p)
+#pragma unroll
+          for (int t = 0; t < D; ++t)
+            v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
+      }
     }
   }
   // stores are unconditional (rows of dead nodes are never read)
@@ -283,6 +288,9 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
   using S = Stage<D, MM, 1 + RG>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
   extern __shared__ double sm[];
+  __shared__ KbSmem<MM> ks;
+  stage_kb_table<MM, TAB>(ks, T);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int team = lane / TEAM, tl = lane - team * TEAM;
   double* st = sm + (size_t)(threadIdx.x >> 5) * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
@@ -341,7 +349,7 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
         live[p] = in[p].perm >= 0;
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
       }
-      stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, T, rows);
+      stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, ks, rows);
 #pragma unroll
       for (int p = 0; p < P; ++p)
         if (live[p]) {
@@ -402,6 +410,9 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   using S = Stage<D, MM, 1, RG * RSTR>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
   extern __shared__ double sm[];
+  __shared__ KbSmem<MM> ks;
+  stage_kb_table<MM, TAB>(ks, T);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int team = lane / TEAM, tl = lane - team * TEAM;
@@ -441,7 +452,7 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
         my_perm[p] = in[p].perm;
       }
-      stage_nodes<D, MM, 1, TAB, P>(in, live, n, T, rows);
+      stage_nodes<D, MM, 1, TAB, P>(in, live, n, ks, rows);
     }
     __syncwarp();
     const int cnt = active ? min(BATCH, ch.count - b0) : 0;

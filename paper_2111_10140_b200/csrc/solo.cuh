@@ -30,8 +30,8 @@ struct SoloCfg {
 };
 
 // window values of one node, dims 0..D-1 in stencil order
-template <int D, int MM, int TAB>
-__device__ __forceinline__ void solo_weights(const double (&nx)[D], const PolyTable& T,
+template <int D, int MM>
+__device__ __forceinline__ void solo_weights(const double (&nx)[D], const KbSmem<MM>& ks,
                                              double (&wt)[D][2 * MM], int& u_last, int n) {
   constexpr int W = 2 * MM;
   double x[D];
@@ -48,10 +48,13 @@ __device__ __forceinline__ void solo_weights(const double (&nx)[D], const PolyTa
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
+    for (int ip = 0; ip < MM; ++ip) {
+      const double2 c = lds_volatile2(&ks.c[k][ip]);
 #pragma unroll
-      for (int t = 0; t < D; ++t) v[i][t] = k == kPolyTerms - 1 ? c : fma(v[i][t], x[t], c);
+      for (int t = 0; t < D; ++t) {
+        v[2 * ip][t] = k == kPolyTerms - 1 ? c.x : fma(v[2 * ip][t], x[t], c.x);
+        v[2 * ip + 1][t] = k == kPolyTerms - 1 ? c.y : fma(v[2 * ip + 1][t], x[t], c.y);
+      }
     }
   }
 #pragma unroll
@@ -138,6 +141,9 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
                                                      int64_t rhs_stride) {
   using C = SoloCfg<D, MM>;
   constexpr int W = C::W, LINES = C::LINES, NACC = C::NACC;
+  __shared__ KbSmem<MM> ks;
+  stage_kb_table<MM, TAB>(ks, T);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= sv.nchunks) return;   // warp-uniform
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
     pipe.advance(sv, ch, q, nx, a, alpha, lda, nr);
     double wt[D][W];
     int u;
-    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
+    solo_weights<D, MM>(nx, ks, wt, u, n);
     if (cur == INT_MIN) cur = u;
     if (u != cur) move_to(cur, u);
 #pragma unroll
@@ -276,6 +282,9 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
                                                      double* __restrict__ out, int64_t ldo) {
   using C = SoloCfg<D, MM>;
   constexpr int W = C::W, LINES = C::LINES;
+  __shared__ KbSmem<MM> ks;
+  stage_kb_table<MM, TAB>(ks, T);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= sv.nchunks) return;
@@ -309,7 +318,7 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
     double wt[D][W];
     int u;
-    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
+    solo_weights<D, MM>(nx, ks, wt, u, n);
     if (u != cur) {
       if (PREFETCH && u == cur + 1) {
         // one-cell move: the entering cell was prefetched into `ahead`
