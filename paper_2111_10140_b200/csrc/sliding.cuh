@@ -220,11 +220,18 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
   // all W*P*D Horner chains advance together (k outer): W*P*D independent FMAs per step
   // hide the DFMA latency, and each coefficient is materialised once for P*D uses
   double v[W][P][D];
+  double2 cur[MM], nxt[MM];   // coefficient row k+1 in flight during row k (see solo.cuh)
+#pragma unroll
+  for (int ip = 0; ip < MM; ++ip) cur[ip] = lds_volatile2(&ks.c[kPolyTerms - 1][ip]);
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
+    if (k > 0) {
+#pragma unroll
+      for (int ip = 0; ip < MM; ++ip) nxt[ip] = lds_volatile2(&ks.c[k - 1][ip]);
+    }
 #pragma unroll
     for (int ip = 0; ip < MM; ++ip) {
-      const double2 c2 = lds_volatile2(&ks.c[k][ip]);
+      const double2 c2 = cur[ip];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = 2 * ip + h;
@@ -235,6 +242,10 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
           for (int t = 0; t < D; ++t)
             v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
       }
+    }
+    if (k > 0) {
+#pragma unroll
+      for (int ip = 0; ip < MM; ++ip) cur[ip] = nxt[ip];
     }
   }
   // stores are unconditional (rows of dead nodes are never read)

@@ -45,16 +45,29 @@ __device__ __forceinline__ void solo_weights(const double (&nx)[D], const KbSmem
     if (t == D - 1) u_last = wrap_cell((int)fl, n);
   }
   double v[W][D];
+  // coefficient row k+1 is in flight while the FMAs of row k run (volatile loads stay in
+  // program order, so the pipelining is explicit)
+  double2 cur[MM], nxt[MM];
+#pragma unroll
+  for (int ip = 0; ip < MM; ++ip) cur[ip] = lds_volatile2(&ks.c[kPolyTerms - 1][ip]);
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
+    if (k > 0) {
+#pragma unroll
+      for (int ip = 0; ip < MM; ++ip) nxt[ip] = lds_volatile2(&ks.c[k - 1][ip]);
+    }
 #pragma unroll
     for (int ip = 0; ip < MM; ++ip) {
-      const double2 c = lds_volatile2(&ks.c[k][ip]);
+      const double2 c = cur[ip];
 #pragma unroll
       for (int t = 0; t < D; ++t) {
         v[2 * ip][t] = k == kPolyTerms - 1 ? c.x : fma(v[2 * ip][t], x[t], c.x);
         v[2 * ip + 1][t] = k == kPolyTerms - 1 ? c.y : fma(v[2 * ip + 1][t], x[t], c.y);
       }
+    }
+    if (k > 0) {
+#pragma unroll
+      for (int ip = 0; ip < MM; ++ip) cur[ip] = nxt[ip];
     }
   }
 #pragma unroll
