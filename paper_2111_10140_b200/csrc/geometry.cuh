@@ -43,32 +43,6 @@ void free_sorted_side(SortedSide* s);
 void make_poly_table(int m, double b, PolyTable* t);
 int kb_table_id(int M, int n);   // 1: n = 2M, 2: 2n = 3M, 0: run-time table
 
-// Coefficient table in shared memory, [k][i/2] pairs (i = stencil offset), staged once per
-// CTA.  Reads go through ld.volatile.shared so ptxas can neither hoist all 14*2m
-// coefficients into registers nor re-materialise each double with two MOVs: one
-// broadcast LDS.128 feeds 2*(nodes x dims) FMAs.
-template <int MM>
-struct KbSmem {
-  double2 c[kPolyTerms][MM];
-};
-
-template <int MM, int TAB>
-__device__ __forceinline__ void stage_kb_table(KbSmem<MM>& s, const PolyTable& T) {
-  // TAB is kept for the launch interface; every kernel reads the plan's table T
-  for (int e = threadIdx.x; e < kPolyTerms * MM; e += blockDim.x) {
-    const int k = e / MM, ip = e - k * MM;
-    s.c[k][ip] = make_double2(T.c[2 * ip][k], T.c[2 * ip + 1][k]);
-  }
-}
-
-__device__ __forceinline__ double2 lds_volatile2(const double2* p) {
-  double2 r;
-  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];"
-               : "=d"(r.x), "=d"(r.y)
-               : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return r;
-}
-
 // ---------------------------------------------------------------------------
 // device: per-dimension window values of one node in the 2m stencil order
 // ---------------------------------------------------------------------------

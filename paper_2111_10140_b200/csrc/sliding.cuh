@@ -193,7 +193,7 @@ struct Round {
 // the mirrored stencil position.
 template <int D, int MM, int EXTRA, int TAB, int P>
 __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool (&live)[P], int n,
-                                            const KbSmem<MM>& ks, double* const (&row)[P]) {
+                                            const PolyTable& T, double* const (&row)[P]) {
   constexpr int W = 2 * MM;
   double x[P][D];
   int pos0[P][D];   // store position of offset 0; step +1 or -1 (mirrored)
@@ -220,32 +220,16 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
   // all W*P*D Horner chains advance together (k outer): W*P*D independent FMAs per step
   // hide the DFMA latency, and each coefficient is materialised once for P*D uses
   double v[W][P][D];
-  double2 cur[MM], nxt[MM];   // coefficient row k+1 in flight during row k (see solo.cuh)
-#pragma unroll
-  for (int ip = 0; ip < MM; ++ip) cur[ip] = lds_volatile2(&ks.c[kPolyTerms - 1][ip]);
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
-    if (k > 0) {
 #pragma unroll
-      for (int ip = 0; ip < MM; ++ip) nxt[ip] = lds_volatile2(&ks.c[k - 1][ip]);
-    }
+    for (int i = 0; i < W; ++i) {
+      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
 #pragma unroll
-    for (int ip = 0; ip < MM; ++ip) {
-      const double2 c2 = cur[ip];
+      for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * ip + h;
-        const double c = h ? c2.y : c2.x;
-#pragma unroll
-        for (int p = 0; p < P; ++p)
-#pragma unroll
-          for (int t = 0; t < D; ++t)
-            v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
-      }
-    }
-    if (k > 0) {
-#pragma unroll
-      for (int ip = 0; ip < MM; ++ip) cur[ip] = nxt[ip];
+        for (int t = 0; t < D; ++t)
+          v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
     }
   }
   // stores are unconditional (rows of dead nodes are never read)
@@ -299,9 +283,6 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
   using S = Stage<D, MM, 1 + RG>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
   extern __shared__ double sm[];
-  __shared__ KbSmem<MM> ks;
-  stage_kb_table<MM, TAB>(ks, T);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int team = lane / TEAM, tl = lane - team * TEAM;
   double* st = sm + (size_t)(threadIdx.x >> 5) * S::WARP_SPAN + (size_t)team * S::TEAM_SPAN;
@@ -360,7 +341,7 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
         live[p] = in[p].perm >= 0;
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
       }
-      stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, ks, rows);
+      stage_nodes<D, MM, 1 + RG, TAB, P>(in, live, n, T, rows);
 #pragma unroll
       for (int p = 0; p < P; ++p)
         if (live[p]) {
@@ -421,9 +402,6 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
   using S = Stage<D, MM, 1, RG * RSTR>;
   constexpr int W = C::W, TEAM = C::TEAM, LPL = C::LPL, TPW = C::TPW;
   extern __shared__ double sm[];
-  __shared__ KbSmem<MM> ks;
-  stage_kb_table<MM, TAB>(ks, T);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int team = lane / TEAM, tl = lane - team * TEAM;
@@ -463,7 +441,7 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
         rows[p] = st + (tl + TEAM * p) * S::STRIDE;
         my_perm[p] = in[p].perm;
       }
-      stage_nodes<D, MM, 1, TAB, P>(in, live, n, ks, rows);
+      stage_nodes<D, MM, 1, TAB, P>(in, live, n, T, rows);
     }
     __syncwarp();
     const int cnt = active ? min(BATCH, ch.count - b0) : 0;

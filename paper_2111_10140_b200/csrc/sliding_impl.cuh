@@ -63,7 +63,7 @@ template <int D, int MM, int TAB>
 static bool spread_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
                        cudaStream_t s) {
-  if constexpr (SoloFits<D, MM, 2>::value) {
+  if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
     if (nr >= 2) {
       run_spread_solo<D, MM, 2, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
       return true;
@@ -75,7 +75,7 @@ static bool spread_tab(const SortedSide& sv, const Window& w, int n, const PolyT
       return true;
     }
   }
-  if constexpr (Fits<D, MM, 2>::value && MM <= 4) {
+  if constexpr (Fits<D, MM, 2>::value && MM <= 4 && TAB != 0) {
     if (nr >= 2) {
       run_spread_v2<D, MM, 2, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
       return true;
@@ -94,7 +94,8 @@ template <int D, int MM>
 static bool spread_mm(const SortedSide& sv, const Window& w, int n, int tab, const PolyTable& T,
                       const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
                       cudaStream_t s) {
-  (void)tab;   // all kernels read the plan's coefficient table (staged in shared memory)
+  if (tab == 1) return spread_tab<D, MM, 1>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
+  if (tab == 2) return spread_tab<D, MM, 2>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
   return spread_tab<D, MM, 0>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
 }
 
@@ -102,7 +103,7 @@ template <int D, int MM, int TAB>
 static bool gather_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                        cudaStream_t s) {
-  if constexpr (SoloFits<D, MM, 2>::value) {
+  if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
     if (nr >= 2) {
       run_gather_solo<D, MM, 2, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);
       return true;
@@ -114,7 +115,7 @@ static bool gather_tab(const SortedSide& sv, const Window& w, int n, const PolyT
       return true;
     }
   }
-  if constexpr (Fits<D, MM, 2>::value && MM <= 4) {
+  if constexpr (Fits<D, MM, 2>::value && MM <= 4 && TAB != 0) {
     if (nr >= 2) {
       run_gather_v2<D, MM, 2, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);
       return true;
@@ -133,7 +134,8 @@ template <int D, int MM>
 static bool gather_mm(const SortedSide& sv, const Window& w, int n, int tab, const PolyTable& T,
                       const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                       cudaStream_t s) {
-  (void)tab;
+  if (tab == 1) return gather_tab<D, MM, 1>(sv, w, n, T, grid, rs, nr, out, ldo, s);
+  if (tab == 2) return gather_tab<D, MM, 2>(sv, w, n, T, grid, rs, nr, out, ldo, s);
   return gather_tab<D, MM, 0>(sv, w, n, T, grid, rs, nr, out, ldo, s);
 }
 

@@ -30,8 +30,8 @@ struct SoloCfg {
 };
 
 // window values of one node, dims 0..D-1 in stencil order
-template <int D, int MM>
-__device__ __forceinline__ void solo_weights(const double (&nx)[D], const KbSmem<MM>& ks,
+template <int D, int MM, int TAB>
+__device__ __forceinline__ void solo_weights(const double (&nx)[D], const PolyTable& T,
                                              double (&wt)[D][2 * MM], int& u_last, int n) {
   constexpr int W = 2 * MM;
   double x[D];
@@ -45,29 +45,13 @@ __device__ __forceinline__ void solo_weights(const double (&nx)[D], const KbSmem
     if (t == D - 1) u_last = wrap_cell((int)fl, n);
   }
   double v[W][D];
-  // coefficient row k+1 is in flight while the FMAs of row k run (volatile loads stay in
-  // program order, so the pipelining is explicit)
-  double2 cur[MM], nxt[MM];
-#pragma unroll
-  for (int ip = 0; ip < MM; ++ip) cur[ip] = lds_volatile2(&ks.c[kPolyTerms - 1][ip]);
 #pragma unroll
   for (int k = kPolyTerms - 1; k >= 0; --k) {
-    if (k > 0) {
 #pragma unroll
-      for (int ip = 0; ip < MM; ++ip) nxt[ip] = lds_volatile2(&ks.c[k - 1][ip]);
-    }
+    for (int i = 0; i < W; ++i) {
+      const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
 #pragma unroll
-    for (int ip = 0; ip < MM; ++ip) {
-      const double2 c = cur[ip];
-#pragma unroll
-      for (int t = 0; t < D; ++t) {
-        v[2 * ip][t] = k == kPolyTerms - 1 ? c.x : fma(v[2 * ip][t], x[t], c.x);
-        v[2 * ip + 1][t] = k == kPolyTerms - 1 ? c.y : fma(v[2 * ip + 1][t], x[t], c.y);
-      }
-    }
-    if (k > 0) {
-#pragma unroll
-      for (int ip = 0; ip < MM; ++ip) cur[ip] = nxt[ip];
+      for (int t = 0; t < D; ++t) v[i][t] = k == kPolyTerms - 1 ? c : fma(v[i][t], x[t], c);
     }
   }
 #pragma unroll
@@ -154,9 +138,6 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
                                                      int64_t rhs_stride) {
   using C = SoloCfg<D, MM>;
   constexpr int W = C::W, LINES = C::LINES, NACC = C::NACC;
-  __shared__ KbSmem<MM> ks;
-  stage_kb_table<MM, TAB>(ks, T);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= sv.nchunks) return;   // warp-uniform
@@ -212,7 +193,7 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
     pipe.advance(sv, ch, q, nx, a, alpha, lda, nr);
     double wt[D][W];
     int u;
-    solo_weights<D, MM>(nx, ks, wt, u, n);
+    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
     if (cur == INT_MIN) cur = u;
     if (u != cur) move_to(cur, u);
 #pragma unroll
@@ -295,9 +276,6 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
                                                      double* __restrict__ out, int64_t ldo) {
   using C = SoloCfg<D, MM>;
   constexpr int W = C::W, LINES = C::LINES;
-  __shared__ KbSmem<MM> ks;
-  stage_kb_table<MM, TAB>(ks, T);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ci >= sv.nchunks) return;
@@ -331,7 +309,7 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
     double wt[D][W];
     int u;
-    solo_weights<D, MM>(nx, ks, wt, u, n);
+    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
     if (u != cur) {
       if (PREFETCH && u == cur + 1) {
         // one-cell move: the entering cell was prefetched into `ahead`
