@@ -281,23 +281,23 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
   if (ci >= sv.nchunks) return;
   const Chunk ch = sv.chunks[ci];
   const double* g = grid + w.grid_off;
-  int64_t rowoff[LINES];
-#pragma unroll
-  for (int a = 0; a < LINES; ++a)
-    rowoff[a] = D == 2 ? (int64_t)wrap_cell(ch.col - MM + 1 + a, n) * n : 0;
+  // grid index of (line a, cell c); row offsets are recomputed, not kept (registers)
+  auto cell_index = [&](int a, int c) -> int64_t {
+    return rowoff_dyn<D, MM>(ch.col, a, n) + wrap_cell(c, n);
+  };
 
   double gv[LINES][W][RG];
-  // grid column of cell cur + MM + 1, prefetched when registers allow (2-D windows are at
-  // the 255-register limit already and rarely move their window)
-  constexpr bool PREFETCH = C::NACC * RG <= 16;
+  // entering column for a one-cell move, loaded one node ahead (the input pipeline already
+  // holds the next node's coordinates, so the move is known before it is needed)
   double ahead[LINES][RG];
+  int ahead_cell = INT_MIN;
   auto load_slot = [&](int k, int c) {
-    const int cm = wrap_cell(c, n);
 #pragma unroll
-    for (int a = 0; a < LINES; ++a)
+    for (int a = 0; a < LINES; ++a) {
+      const int64_t ix = cell_index(a, c);
 #pragma unroll
-      for (int r = 0; r < RG; ++r)
-        gv[a][k][r] = r < nr ? __ldg(g + r * rhs_stride + rowoff[a] + cm) : 0.0;
+      for (int r = 0; r < RG; ++r) gv[a][k][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
+    }
   };
   int cur = INT_MIN;
   const int count = ch.count;
@@ -307,12 +307,10 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     double nx[D];
     double prior[RG];   // out[perm] before this window (each node is written once)
     const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
-    double wt[D][W];
-    int u;
-    solo_weights<D, MM, TAB>(nx, T, wt, u, n);
+    const int u = wrap_cell((int)floor(nx[D - 1]), n);
     if (u != cur) {
-      if (PREFETCH && u == cur + 1) {
-        // one-cell move: the entering cell was prefetched into `ahead`
+      if (u == cur + 1 && ahead_cell == u + MM) {
+        // one-cell move: the entering cell was loaded during the previous node
 #pragma unroll
         for (int a = 0; a < LINES; ++a)
 #pragma unroll
@@ -338,15 +336,25 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
         for (int k = 0; k < W; ++k) load_slot(k, u - MM + 1 + k);
       }
       cur = u;
-      if (PREFETCH) {
-        const int cm = wrap_cell(u + MM + 1, n);
+    }
+    // look ahead: if this lane's next node sits one cell further, start loading its column
+    // (skipped for 2-D windows: their 64-value window already fills the register file)
+    constexpr bool LOOKAHEAD = C::NACC * RG <= 32;
+    if (LOOKAHEAD && q + 32 < count) {
+      const int un = wrap_cell((int)floor(pipe.nx1[D - 1]), n);
+      if (un == cur + 1 && ahead_cell != un + MM) {
+        ahead_cell = un + MM;
 #pragma unroll
-        for (int a = 0; a < LINES; ++a)
+        for (int a = 0; a < LINES; ++a) {
+          const int64_t ix = cell_index(a, ahead_cell);
 #pragma unroll
-          for (int r = 0; r < RG; ++r)
-            ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + rowoff[a] + cm) : 0.0;
+          for (int r = 0; r < RG; ++r) ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
+        }
       }
     }
+    double wt[D][W];
+    int u_w;
+    solo_weights<D, MM, TAB>(nx, T, wt, u_w, n);
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
       double s = 0.0;
