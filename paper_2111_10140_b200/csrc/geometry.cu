@@ -47,10 +47,14 @@ __global__ void k_column_counts(const uint64_t* __restrict__ key, int64_t N, uin
   if (live && (int)(threadIdx.x & 31) == leader) atomicAdd(&counts[col], __popc(peers));
 }
 
-static int chunk_cap_for(int d) {
-  // d = 3: one 32-lane team per run; d <= 2: one warp per run, 32 nodes per lane
+static int chunk_cap_for(int d, int64_t N) {
+  // d = 3: one 32-lane team per run; d <= 2: one warp per run, 32 nodes per lane.
+  // Up to 1024 nodes per run amortise the window flushes; small windows use shorter
+  // runs so that a launch still has >= ~8 warps per SM (148 SMs).
   (void)d;
-  return 1024;
+  int64_t cap = N / (148 * 8);
+  cap = (cap + 31) / 32 * 32;
+  return (int)std::max<int64_t>(64, std::min<int64_t>(1024, cap));
 }
 
 void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
@@ -99,7 +103,7 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
     AFS_CUDA(cudaGetLastError());
     std::vector<int32_t> hc(ncol);
     AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * ncol, cudaMemcpyDeviceToHost));
-    const int cap = chunk_cap_for(d);
+    const int cap = chunk_cap_for(d, N);
     std::vector<Chunk> ch;
     int64_t pos = 0;
     for (int64_t c = 0; c < ncol; ++c) {
