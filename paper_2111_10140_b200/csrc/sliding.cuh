@@ -360,36 +360,20 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
         cur = u;
       }
       do {
-        // two nodes of the run per iteration when possible: the second node's shared-memory
-        // loads overlap the first node's FMAs (no loop-carried register copies)
         const double* row = st + q * S::STRIDE;
-        const bool pair = q + 1 < cnt &&
-                          (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) == cur;
-        const int nq = pair ? 2 : 1;
-        q += nq;
-        u = q < cnt ? (int)__double_as_longlong(st[q * S::STRIDE + S::U_OFF]) : INT_MIN;
-        double wl[2][W], pw[2][LPL][RG];
+        ++q;
+        u = q < cnt ? (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) : INT_MIN;
+        double wl[W];
+        load_last<W>(row + (D - 1) * W, wl);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !pair) break;
-          const double* rh = row + h * S::STRIDE;
-          load_last<W>(rh + (D - 1) * W, wl[h]);
+        for (int j = 0; j < LPL; ++j) {
+          const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
-          for (int j = 0; j < LPL; ++j) {
-            const double lw = line_weight<D, MM>(rh, lg[j]);
+          for (int r = 0; r < RG; ++r) {
+            const double p = lw * row[S::A_OFF + r];
 #pragma unroll
-            for (int r = 0; r < RG; ++r) pw[h][j][r] = lw * rh[S::A_OFF + r];
+            for (int k = 0; k < W; ++k) acc[j][k][r] = fma(p, wl[k], acc[j][k][r]);
           }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !pair) break;
-#pragma unroll
-          for (int j = 0; j < LPL; ++j)
-#pragma unroll
-            for (int r = 0; r < RG; ++r)
-#pragma unroll
-              for (int k = 0; k < W; ++k) acc[j][k][r] = fma(pw[h][j][r], wl[h][k], acc[j][k][r]);
         }
       } while (u == cur);
     }
@@ -496,49 +480,32 @@ __global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Wi
           for (int r = 0; r < RG; ++r) ahead[j][r] = load_cell(u + MM + 1, j, r);
       }
       do {
-        // two nodes of the run per iteration when possible (see the spread)
         const double* row = st + q * S::STRIDE;
-        const bool pair = q + 1 < cnt &&
-                          (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) == cur;
-        const int qq = q;
-        q += pair ? 2 : 1;
-        u = q < cnt ? (int)__double_as_longlong(st[q * S::STRIDE + S::U_OFF]) : INT_MIN;
-        double wl[2][W], lw[2][LPL];
+        const int qq = q++;
+        u = q < cnt ? (int)__double_as_longlong(row[S::STRIDE + S::U_OFF]) : INT_MIN;
+        double wl[W];
+        load_last<W>(row + (D - 1) * W, wl);
+        double part[RG];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !pair) break;
-          const double* rh = row + h * S::STRIDE;
-          load_last<W>(rh + (D - 1) * W, wl[h]);
+        for (int r = 0; r < RG; ++r) part[r] = 0.0;
 #pragma unroll
-          for (int j = 0; j < LPL; ++j) lw[h][j] = line_weight<D, MM>(rh, lg[j]);
-        }
-        double part[2][RG];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !pair) break;
+        for (int j = 0; j < LPL; ++j) {
+          const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
           for (int r = 0; r < RG; ++r) {
-            part[h][r] = 0.0;
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-            for (int j = 0; j < LPL; ++j) {
-              double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-              for (int k = 0; k < W; k += 2) {
-                s0 = fma(wl[h][k], gv[j][k][r], s0);
-                if (k + 1 < W) s1 = fma(wl[h][k + 1], gv[j][k + 1][r], s1);
-              }
-              part[h][r] = fma(lw[h][j], s0 + s1, part[h][r]);
+            for (int k = 0; k < W; k += 2) {
+              s0 = fma(wl[k], gv[j][k][r], s0);
+              if (k + 1 < W) s1 = fma(wl[k + 1], gv[j][k + 1][r], s1);
             }
+            part[r] = fma(lw, s0 + s1, part[r]);
           }
         }
-        __syncwarp(team_mask);   // every lane of the team is done reading rows qq, qq+1
+        __syncwarp(team_mask);   // every lane of the team is done reading row qq
+        double* prow = st + qq * S::STRIDE;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !pair) break;
-          double* prow = st + (qq + h) * S::STRIDE;
-#pragma unroll
-          for (int r = 0; r < RG; ++r) prow[r * RSTR + tl] = part[h][r];
-        }
+        for (int r = 0; r < RG; ++r) prow[r * RSTR + tl] = part[r];
       } while (u == cur);
     }
     __syncwarp();
