@@ -143,6 +143,25 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_fp64_peak():
+    """fp64 FMA peak measured by tools/fp64_peak.cu on this pool (profiles/r01_fp64_peak.txt)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_fp64_peak.txt")) as fh:
+            vals = [float(l.split("=")[1].split("TFLOP")[0]) for l in fh if "TFLOP/s" in l]
+        return max(vals), "measured (profiles/r01_fp64_peak.txt, DFMA microbenchmark)"
+    except Exception:
+        return 37.0, "nominal (B200 fp64 spec)"
+
+
+def ncu_traffic(key):
+    """dram read+write bytes per launch from a committed ncu --set full capture."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # CPU side: oracle port timed on the host (never the product path)
 # ---------------------------------------------------------------------------
@@ -283,9 +302,12 @@ def run_ours(args):
         plan.apply_device(alpha, out, 1)
     torch.cuda.synchronize()
     st = plan.stage_times(reset=True)
+    win_sp, win_ga = plan.window_times(reset=True)
     plan.set_profiling(False)
     napp = max(1, st["applies"])
     stage = {k: st[k] / napp for k in ("spread_ms", "spectral_ms", "gather_ms")}
+    win_sp = [t / napp for t in win_sp]
+    win_ga = [t / napp for t in win_ga]
 
     # --- e2e through the public API with host buffers (numpy in, numpy out)
     e2e_times = []
@@ -307,12 +329,24 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
-    # roofline of the dominant stage on this rank (algorithmic bytes of its windows)
+    # roofline of the dominant kernel: group the per-window launches by (stage, window dim),
+    # take the group with the largest total time, report algorithmic bytes per launch over
+    # its mean launch time (and its fp64 rate against the measured fp64 peak)
     peak, peak_src = measured_peak_hbm()
-    B, Bs, Bg = algorithmic_bytes(w.N, my_windows, plan.n)
-    dom = max(stage, key=stage.get)
-    dom_bytes = {"spread_ms": Bs, "gather_ms": Bg, "spectral_ms": sum(16 * plan.n ** len(x) for x in my_windows)}[dom]
-    achieved = dom_bytes / (stage[dom] * 1e-3) / 1e9
+    groups = {}
+    for l, win in enumerate(my_windows):
+        d = len(win)
+        for kind, t in (("spread", win_sp[l]), ("gather", win_ga[l])):
+            groups.setdefault((kind, d), []).append(t)
+    (kind, d), times = max(groups.items(), key=lambda kv: sum(kv[1]))
+    t_launch = float(np.mean(times)) * 1e-3
+    n = plan.n
+    dom_bytes = w.N * 8 * d + w.N * 8 + 8 * n ** d      # coordinates + alpha/out + grid
+    achieved = dom_bytes / t_launch / 1e9
+    fma_per_node = (2 * w.m) ** d + 2 * w.m * d * 13 + (2 * w.m) ** (d - 1)   # touches + Horner
+    fp64_tflops = 2.0 * fma_per_node * w.N / t_launch / 1e12
+    fp64_peak, fp64_src = measured_fp64_peak()
+    traffic = ncu_traffic(f"{kind}_d{d}")
     info = plan.info()
     Btot, _, _ = algorithmic_bytes(w.N, w.windows, plan.n)
 
@@ -341,12 +375,17 @@ def run_ours(args):
                                     "achieved_gbs": Btot / (ms_step * 1e-3) / 1e9,
                                     "frac_of_measured": Btot / (ms_step * 1e-3) / 1e9 / peak},
             "stage_ms": stage,
-            "roofline": {"bound": "hbm", "kernel": dom.replace("_ms", ""),
+            "roofline": {"bound": "hbm", "kernel": f"{kind} ({d}-D windows)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": dom_bytes,
-                         "note": "stage = all windows of this rank; fp64-issue is the binding "
-                                 "limit at m=4 (DESIGN.md)"},
+                         "mean_launch_ms": t_launch * 1e3, "launches_per_step": len(times),
+                         "fp64": {"achieved_tflops": fp64_tflops, "peak_tflops": fp64_peak,
+                                  "frac": fp64_tflops / fp64_peak, "peak_source": fp64_src,
+                                  "fma_per_node": fma_per_node},
+                         "note": "m=4 makes the kernel fp64-issue-bound (DESIGN.md §5); "
+                                 "traffic = ncu dram read+write per launch (profiles/)"},
+            "window_ms": {"spread": win_sp, "gather": win_ga},
             "cpu_baseline": cpu,
             "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * w.N,
                     "d2h_bytes_per_step": 8 * w.N,

@@ -134,6 +134,9 @@ int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles
  * and resets the accumulators when reset != 0. */
 int afs_plan_set_profiling(afs_plan* plan, int32_t enable);
 int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset);
+/* Per-window kernel time of the spread and the gather (ms accumulated over profiled
+ * applies; arrays of n_windows). */
+int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, int32_t reset);
 
 /* Solve (K + beta I) x = b by plain CG from x0 = 0 (krr.py:76-110).
  * Requires n_targets == n_sources (no separate targets).  b, x: device.

@@ -102,6 +102,9 @@ struct afs_plan {
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};
+  // per-window kernel timing in profiling mode: events bracket each window's launches
+  std::vector<cudaEvent_t> wev_spread, wev_gather;     // P + 1 each
+  std::vector<double> win_ms_spread, win_ms_gather;    // accumulated, per window
   int64_t profiled_applies = 0;
   std::mutex mu;
 };

@@ -112,6 +112,16 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
   }
   for (int i = 0; i < 4; ++i)
     if (!p->ev[i]) AFS_CUDA(cudaEventCreate(&p->ev[i]));
+  if (p->wev_spread.empty()) {
+    p->wev_spread.resize(p->P + 1);
+    p->wev_gather.resize(p->P + 1);
+    for (int i = 0; i <= p->P; ++i) {
+      AFS_CUDA(cudaEventCreate(&p->wev_spread[i]));
+      AFS_CUDA(cudaEventCreate(&p->wev_gather[i]));
+    }
+    p->win_ms_spread.assign(p->P, 0.0);
+    p->win_ms_gather.assign(p->P, 0.0);
+  }
   AFS_CUDA(cudaEventRecord(p->ev[0], s));
   spread_all(p, alpha, lda, R, s);
   AFS_CUDA(cudaEventRecord(p->ev[1], s));
@@ -124,6 +134,15 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
     float ms = 0.f;
     AFS_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
     p->stage_ms[i] += ms;
+  }
+  if (p->window_eval == 0) {
+    for (int l = 0; l < p->P; ++l) {
+      float ms = 0.f;
+      AFS_CUDA(cudaEventElapsedTime(&ms, p->wev_spread[l], p->wev_spread[l + 1]));
+      p->win_ms_spread[l] += ms;
+      AFS_CUDA(cudaEventElapsedTime(&ms, p->wev_gather[l], p->wev_gather[l + 1]));
+      p->win_ms_gather[l] += ms;
+    }
   }
   p->profiled_applies += 1;
 }
@@ -148,6 +167,8 @@ static void free_plan(afs_plan* p) {
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (afs::GraphEntry& g : p->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (cudaEvent_t e : p->wev_spread) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->wev_gather) cudaEventDestroy(e);
   if (p->istream) cudaStreamDestroy(p->istream);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
@@ -392,6 +413,21 @@ int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset) {
     if (reset) {
       for (int i = 0; i < 3; ++i) plan->stage_ms[i] = 0.0;
       plan->profiled_applies = 0;
+    }
+  });
+}
+
+int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, int32_t reset) {
+  return afs::guarded([&] {
+    if (!plan || !spread_ms || !gather_ms) throw afs::Error(AFS_ERR_VALIDATION, "null argument");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    for (int l = 0; l < plan->P; ++l) {
+      spread_ms[l] = plan->win_ms_spread.empty() ? 0.0 : plan->win_ms_spread[l];
+      gather_ms[l] = plan->win_ms_gather.empty() ? 0.0 : plan->win_ms_gather[l];
+    }
+    if (reset && !plan->win_ms_spread.empty()) {
+      plan->win_ms_spread.assign(plan->P, 0.0);
+      plan->win_ms_gather.assign(plan->P, 0.0);
     }
   });
 }

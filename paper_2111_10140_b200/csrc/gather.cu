@@ -138,8 +138,12 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
   if (p->window_eval != 0) {
     gather_v1(p, 0, p->P, out, ldo, R, s);
   } else {
-    for (int l = 0; l < p->P; ++l)
+    const bool timed = p->profiling && !p->wev_gather.empty();
+    for (int l = 0; l < p->P; ++l) {
+      if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
       if (!gather_v2_window(p, l, out, ldo, R, s)) gather_v1(p, l, l + 1, out, ldo, R, s);
+    }
+    if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
   }
   AFS_CUDA(cudaGetLastError());
 }

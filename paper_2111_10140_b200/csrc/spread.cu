@@ -118,8 +118,10 @@ int v2_rhs_group(int D, int m, int R) {
 
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
   AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * p->grid_total * R, s));
+  const bool timed = p->profiling && !p->wev_spread.empty();
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
+    if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[l], s));
     if (spread_v2_window(p, l, alpha, lda, R, s)) continue;
     switch (p->m) {
       case 1: launch_spread_m<1>(p, w, alpha, lda, R, s); break;
@@ -132,6 +134,7 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
       default: launch_spread_m<8>(p, w, alpha, lda, R, s); break;
     }
   }
+  if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   AFS_CUDA(cudaGetLastError());
 }
 

@@ -244,6 +244,14 @@ class _Plan:
         return {"spread_ms": buf[0], "spectral_ms": buf[1], "gather_ms": buf[2],
                 "applies": int(buf[3])}
 
+    def window_times(self, reset: bool = True):
+        """Per-window (spread_ms, gather_ms) lists accumulated over profiled applies."""
+        P = len(self.windows)
+        sp = (ctypes.c_double * P)()
+        ga = (ctypes.c_double * P)()
+        _native.check(self.lib.afs_plan_window_times(self.handle, sp, ga, 1 if reset else 0))
+        return list(sp), list(ga)
+
     def close(self):
         h = getattr(self, "handle", None)
         if h:
