@@ -96,6 +96,7 @@ struct afs_plan {
   std::vector<afs::SortedSide*> src_side, tgt_side;
   afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
   bool use_graphs = true;
+  int fft_mode = 0;                    // 0 four-step register FFT where n allows, 1 generic line kernel
   std::vector<afs::GraphEntry> graphs;
   cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;

@@ -4,6 +4,8 @@
 #include <cstring>
 
 #include "afs_internal.cuh"
+
+#include <cstdlib>
 #include "geometry.cuh"
 
 namespace afs {
@@ -284,6 +286,10 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
     if (d->window_eval != 0 && d->window_eval != 1)
       throw Error(AFS_ERR_VALIDATION, "window_eval must be 0 (polynomial) or 1 (exact)");
     p->window_eval = d->window_eval;
+    {   // test hook: AFS_SPECTRAL_GENERIC=1 selects the generic line kernel for every n
+      const char* g = getenv("AFS_SPECTRAL_GENERIC");
+      p->fft_mode = (g && g[0] == '1') ? 1 : 0;
+    }
     if (p->window_eval == 0) {
       p->poly = new PolyTable();
       make_poly_table(p->m, p->b, p->poly);
