@@ -35,7 +35,8 @@ def sources():
 
 
 def headers():
-    return sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [
+    return sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh")) +
+                  glob.glob(os.path.join(PKG, "csrc", "*.inc"))) + [
         os.path.join(REPO, "include", "anovafs.h")]
 
 

@@ -1,6 +1,7 @@
 // Plan-time geometry: per-window scaled node coordinates n*x (nfft.py:170-172
 // with fastsum.py:229 scaling), bin-sorted by base cell with a device radix
 // sort, and cut into column runs ("chunks") for the sliding-window kernels.
+#define AFS_KB_DEFINE   // this translation unit owns the KB coefficient tables (kb_tables.inc)
 #include <cmath>
 #include <cub/cub.cuh>
 
