@@ -91,9 +91,18 @@ def main():
         op._plan.apply_device(al, out, 8)
         st = op._plan.stage_times()
         op._plan.set_profiling(False)
+        # size-independent checks at full N: linearity (rhs 2 = rhs 0 + rhs 1) and symmetry
+        # <K a0, a1> = <a0, K a1>
+        al[2] = al[0] + al[1]
+        op._plan.apply_device(al, out, 8)
+        lin = float((out[2] - out[0] - out[1]).norm() / out[2].norm())
+        sym = float(abs(torch.dot(out[0], al[1]) - torch.dot(al[0], out[1]))
+                    / (out[0].norm() * al[1].norm()))
         print(json.dumps({"config": "C4", "N": w.N, "R": 8, "ms_per_matvec": ms,
                           "matvec_per_s": 1e3 / ms, "updates_per_s": w.N * 8 * 1e3 / ms,
-                          "plan_build_s": t_build, "stages": st}), flush=True)
+                          "plan_build_s": t_build, "stages": st,
+                          "linearity_rel": lin, "symmetry_rel": sym,
+                          "device_peak_gb": torch.cuda.max_memory_allocated() / 1e9}), flush=True)
         del op, al, out
 
     if "C5" not in skip:
