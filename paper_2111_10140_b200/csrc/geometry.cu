@@ -3,6 +3,7 @@
 // sort, and cut into column runs ("chunks") for the sliding-window kernels.
 #define AFS_KB_DEFINE   // this translation unit owns the KB coefficient tables (kb_tables.inc)
 #include <cmath>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "geometry.cuh"
@@ -37,6 +38,16 @@ __global__ void k_permute_nodes(const double* __restrict__ nx_in, const int32_t*
   for (int t = 0; t < d; ++t) nx_out[t * N + i] = nx_in[t * N + j];
 }
 
+// window origin of every run, so kernels can prefetch a run's grid window from its
+// descriptor alone (same floor/wrap as the kernels apply to nx)
+__global__ void k_chunk_cell0(Chunk* __restrict__ ch, int64_t nch, const double* __restrict__ nx_last,
+                              int n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nch) return;
+  const int c = (int)floor(nx_last[ch[i].begin]);
+  ch[i].cell0 = c < 0 ? c + n : (c >= n ? c - n : c);
+}
+
 __global__ void k_column_counts(const uint64_t* __restrict__ key, int64_t N, uint64_t n,
                                 int32_t* __restrict__ counts) {
   // keys are sorted, so a warp mostly sees one column: aggregate before the atomic
@@ -53,9 +64,11 @@ static int chunk_cap_for(int d, int64_t N) {
   // Up to 1024 nodes per run amortise the window flushes; small windows use shorter
   // runs so that a launch still has >= ~8 warps per SM (148 SMs).
   (void)d;
+  int64_t hi = 1024;
+  if (const char* e = getenv("AFS_CHUNK_CAP_MAX")) hi = std::max(64, atoi(e)) / 32 * 32;   // tuning hook
   int64_t cap = N / (148 * 8);
   cap = (cap + 31) / 32 * 32;
-  return (int)std::max<int64_t>(64, std::min<int64_t>(1024, cap));
+  return (int)std::max<int64_t>(64, std::min<int64_t>(hi, cap));
 }
 
 void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
@@ -109,7 +122,7 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
     int64_t pos = 0;
     for (int64_t c = 0; c < ncol; ++c) {
       for (int32_t o = 0; o < hc[c]; o += cap)
-        ch.push_back(Chunk{(int32_t)c, std::min(cap, hc[c] - o), pos + o});
+        ch.push_back(Chunk{(int32_t)c, std::min(cap, hc[c] - o), pos + o, 0, 0});
       pos += hc[c];
     }
     out->N = N;
@@ -117,6 +130,11 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
     out->chunk_cap = cap;
     AFS_CUDA(cudaMalloc(&out->chunks, sizeof(Chunk) * std::max<size_t>(1, ch.size())));
     AFS_CUDA(cudaMemcpy(out->chunks, ch.data(), sizeof(Chunk) * ch.size(), cudaMemcpyHostToDevice));
+    if (!ch.empty()) {
+      k_chunk_cell0<<<(unsigned)((ch.size() + 255) / 256), 256, 0, s>>>(
+          out->chunks, (int64_t)ch.size(), out->nx + (int64_t)(d - 1) * N, n);
+      AFS_CUDA(cudaGetLastError());
+    }
     p->device_bytes += (int64_t)(sizeof(double) * d + sizeof(int32_t)) * N +
                        (int64_t)sizeof(Chunk) * out->nchunks;
     AFS_CUDA(cudaDeviceSynchronize());

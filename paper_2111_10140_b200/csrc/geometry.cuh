@@ -25,6 +25,8 @@ struct Chunk {
   int32_t col;     // column id: u0*n+u1 (d=3), u0 (d=2), 0 (d=1)
   int32_t count;   // nodes in the run
   int64_t begin;   // first sorted node
+  int32_t cell0;   // last-dim base cell of the first node (filled on the device)
+  int32_t pad_;
 };
 
 // Sorted nodes of one window on one side (sources or targets).

@@ -1,6 +1,8 @@
 // Launch helpers for the v2 kernels; included once per dimension file.
 #pragma once
 
+#include <algorithm>
+
 #include "sliding.cuh"
 #include "solo.cuh"
 
@@ -21,7 +23,18 @@ static void run_gather_solo(const SortedSide& sv, const Window& w, int n, const 
                             const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                             cudaStream_t s) {
   constexpr int threads = 128;
-  const int64_t blocks = (sv.nchunks * 32 + threads - 1) / threads;
+  // persistent warps: at most one resident wave, each warp loops over runs
+  static int resident = 0;
+  if (resident == 0) {
+    int occ = 0, dev = 0, sms = 0;
+    AFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_solo<D, MM, RG, TAB>,
+                                                           threads, 0));
+    AFS_CUDA(cudaGetDevice(&dev));
+    AFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    resident = std::max(1, occ) * sms;
+  }
+  const int64_t need = (sv.nchunks * 32 + threads - 1) / threads;
+  const int64_t blocks = std::min<int64_t>(need, resident);
   k_gather_solo<D, MM, RG, TAB><<<(unsigned)blocks, threads, 0, s>>>(sv, w, n, T, grid, rs, nr,
                                                                     out, ldo);
 }

@@ -267,7 +267,30 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
 
 // ----------------------------------------------------------------------------
 // gather: out[perm] += eta * interp
+//
+// Persistent warps: warp w takes runs w, w + nw, w + 2nw ...  A run's starting window
+// (the stencil around its first node's cell, Chunk::cell0) is copied into shared memory
+// with cp.async while the warp still works on the previous run, so a run starts from
+// shared memory instead of a dependent L2 round trip (ncu: that wait was 30% of the
+// kernel when every warp owned a single run).
 // ----------------------------------------------------------------------------
+template <int D, int MM, int RG>
+__device__ __forceinline__ void solo_window_prefetch(const Chunk& c, const double* g,
+                                                     int64_t rhs_stride, int nr, int n, int lane,
+                                                     double* dst) {
+  using C = SoloCfg<D, MM>;
+  constexpr int W = C::W, NWIN = C::NACC * RG;
+#pragma unroll
+  for (int e = lane; e < NWIN; e += 32) {
+    const int r = e % RG, k = (e / RG) % W, a = e / (RG * W);
+    const int64_t ix = rowoff_dyn<D, MM>(c.col, a, n) + wrap_cell(c.cell0 - MM + 1 + k, n);
+    const double* src = g + (r < nr ? r : 0) * rhs_stride + ix;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + e);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src));
+  }
+  asm volatile("cp.async.commit_group;");
+}
+
 template <int D, int MM, int RG, int TAB>
 __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const Window w, int n,
                                                      const PolyTable T,
@@ -275,101 +298,134 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
                                                      int64_t rhs_stride, int nr,
                                                      double* __restrict__ out, int64_t ldo) {
   using C = SoloCfg<D, MM>;
-  constexpr int W = C::W, LINES = C::LINES;
+  constexpr int W = C::W, LINES = C::LINES, NWIN = C::NACC * RG;
+  __shared__ double s_win[4][2][NWIN];   // per warp: double-buffered starting windows
   const int lane = threadIdx.x & 31;
-  const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ci >= sv.nchunks) return;
-  const Chunk ch = sv.chunks[ci];
+  const int wib = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ci >= sv.nchunks) return;   // warp-uniform
   const double* g = grid + w.grid_off;
-  // grid index of (line a, cell c); row offsets are recomputed, not kept (registers)
-  auto cell_index = [&](int a, int c) -> int64_t {
-    return rowoff_dyn<D, MM>(ch.col, a, n) + wrap_cell(c, n);
-  };
+  // small windows prefetch the entering column into registers, 2-D windows into L1
+  constexpr bool LOOKAHEAD = C::NACC * RG <= 32;
 
-  double gv[LINES][W][RG];
-  // entering column for a one-cell move, loaded one node ahead (the input pipeline already
-  // holds the next node's coordinates, so the move is known before it is needed)
-  double ahead[LINES][RG];
-  int ahead_cell = INT_MIN;
-  auto load_slot = [&](int k, int c) {
-#pragma unroll
-    for (int a = 0; a < LINES; ++a) {
-      const int64_t ix = cell_index(a, c);
-#pragma unroll
-      for (int r = 0; r < RG; ++r) gv[a][k][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
-    }
-  };
-  int cur = INT_MIN;
-  const int count = ch.count;
-  SoloPipe<D, RG> pipe;
-  pipe.prime(sv, ch, lane, out, ldo, nr);
-  for (int q = lane; q < count; q += 32) {
-    double nx[D];
-    double prior[RG];   // out[perm] before this window (each node is written once)
-    const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
-    const int u = wrap_cell((int)floor(nx[D - 1]), n);
-    if (u != cur) {
-      if (u == cur + 1 && ahead_cell == u + MM) {
-        // one-cell move: the entering cell was loaded during the previous node
-#pragma unroll
-        for (int a = 0; a < LINES; ++a)
-#pragma unroll
-          for (int r = 0; r < RG; ++r) {
-#pragma unroll
-            for (int k = 0; k + 1 < W; ++k) gv[a][k][r] = gv[a][k + 1][r];
-            gv[a][W - 1][r] = ahead[a][r];
-          }
-      } else if (cur != INT_MIN && u - cur < W) {
+  Chunk ch = sv.chunks[ci];
+  Chunk chn = ci + nw < sv.nchunks ? sv.chunks[ci + nw] : ch;
+  solo_window_prefetch<D, MM, RG>(ch, g, rhs_stride, nr, n, lane, s_win[wib][0]);
+  int buf = 0;
+
 #pragma unroll 1
-        for (int c = cur; c < u; ++c) {
+  for (; ci < sv.nchunks; ci += nw) {
+    const bool has_next = ci + nw < sv.nchunks;
+    // this run's starting window has landed; start the next run's and its successor's
+    // descriptor
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    double gv[LINES][W][RG];
+#pragma unroll
+    for (int a = 0; a < LINES; ++a)
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+#pragma unroll
+        for (int r = 0; r < RG; ++r) gv[a][k][r] = s_win[wib][buf][(a * W + k) * RG + r];
+    __syncwarp();
+    if (has_next) solo_window_prefetch<D, MM, RG>(chn, g, rhs_stride, nr, n, lane, s_win[wib][buf ^ 1]);
+    const Chunk chnn = ci + 2 * nw < sv.nchunks ? sv.chunks[ci + 2 * nw] : chn;
+
+    // grid index of (line a, cell c); row offsets are recomputed, not kept (registers)
+    auto cell_index = [&](int a, int c) -> int64_t {
+      return rowoff_dyn<D, MM>(ch.col, a, n) + wrap_cell(c, n);
+    };
+    double ahead[LINES][RG];
+    int ahead_cell = INT_MIN;
+    auto load_slot = [&](int k, int c) {
+#pragma unroll
+      for (int a = 0; a < LINES; ++a) {
+        const int64_t ix = cell_index(a, c);
+#pragma unroll
+        for (int r = 0; r < RG; ++r) gv[a][k][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
+      }
+    };
+    int cur = ch.cell0;
+    const int count = ch.count;
+    SoloPipe<D, RG> pipe;
+    pipe.prime(sv, ch, lane, out, ldo, nr);
+#pragma unroll 1
+    for (int q = lane; q < count; q += 32) {
+      double nx[D];
+      double prior[RG];   // out[perm] before this window (each node is written once)
+      const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
+      const int u = wrap_cell((int)floor(nx[D - 1]), n);
+      if (u != cur) {
+        if (LOOKAHEAD && u == cur + 1 && ahead_cell == u + MM) {
+          // one-cell move: the entering cell was loaded during the previous node
 #pragma unroll
           for (int a = 0; a < LINES; ++a)
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
 #pragma unroll
               for (int k = 0; k + 1 < W; ++k) gv[a][k][r] = gv[a][k + 1][r];
+              gv[a][W - 1][r] = ahead[a][r];
             }
-          load_slot(W - 1, c + MM + 1);
+        } else if (u > cur && u - cur < W) {
+#pragma unroll 1
+          for (int c = cur; c < u; ++c) {
+#pragma unroll
+            for (int a = 0; a < LINES; ++a)
+#pragma unroll
+              for (int r = 0; r < RG; ++r) {
+#pragma unroll
+                for (int k = 0; k + 1 < W; ++k) gv[a][k][r] = gv[a][k + 1][r];
+              }
+            load_slot(W - 1, c + MM + 1);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < W; ++k) load_slot(k, u - MM + 1 + k);
         }
-      } else {
-#pragma unroll
-        for (int k = 0; k < W; ++k) load_slot(k, u - MM + 1 + k);
+        cur = u;
       }
-      cur = u;
-    }
-    // look ahead: if this lane's next node sits one cell further, start loading its column
-    // (skipped for 2-D windows: their 64-value window already fills the register file)
-    constexpr bool LOOKAHEAD = C::NACC * RG <= 32;
-    if (LOOKAHEAD && q + 32 < count) {
-      const int un = wrap_cell((int)floor(pipe.nx1[D - 1]), n);
-      if (un == cur + 1 && ahead_cell != un + MM) {
-        ahead_cell = un + MM;
+      // look ahead: if this lane's next node sits one cell further, start loading its column
+      if (q + 32 < count) {
+        const int un = wrap_cell((int)floor(pipe.nx1[D - 1]), n);
+        if (un == cur + 1 && ahead_cell != un + MM) {
+          ahead_cell = un + MM;
 #pragma unroll
-        for (int a = 0; a < LINES; ++a) {
-          const int64_t ix = cell_index(a, ahead_cell);
+          for (int a = 0; a < LINES; ++a) {
+            const int64_t ix = cell_index(a, ahead_cell);
 #pragma unroll
-          for (int r = 0; r < RG; ++r) ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
+            for (int r = 0; r < RG; ++r) {
+              if (LOOKAHEAD) {
+                ahead[a][r] = r < nr ? __ldg(g + r * rhs_stride + ix) : 0.0;
+              } else if (r < nr) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(g + r * rhs_stride + ix));
+              }
+            }
+          }
         }
       }
-    }
-    double wt[D][W];
-    int u_w;
-    solo_weights<D, MM, TAB>(nx, T, wt, u_w, n);
+      double wt[D][W];
+      int u_w;
+      solo_weights<D, MM, TAB>(nx, T, wt, u_w, n);
 #pragma unroll
-    for (int r = 0; r < RG; ++r) {
-      double s = 0.0;
+      for (int r = 0; r < RG; ++r) {
+        double s = 0.0;
 #pragma unroll
-      for (int ln = 0; ln < LINES; ++ln) {
-        double t0 = 0.0, t1 = 0.0;
+        for (int ln = 0; ln < LINES; ++ln) {
+          double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < W; k += 2) {
-          t0 = fma(wt[D - 1][k], gv[ln][k][r], t0);
-          if (k + 1 < W) t1 = fma(wt[D - 1][k + 1], gv[ln][k + 1][r], t1);
+          for (int k = 0; k < W; k += 2) {
+            t0 = fma(wt[D - 1][k], gv[ln][k][r], t0);
+            if (k + 1 < W) t1 = fma(wt[D - 1][k + 1], gv[ln][k + 1][r], t1);
+          }
+          s = D == 2 ? fma(wt[0][ln], t0 + t1, s) : (t0 + t1);
         }
-        s = D == 2 ? fma(wt[0][ln], t0 + t1, s) : (t0 + t1);
+        if (r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, s));
       }
-      if (r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, s));
     }
+    ch = chn;
+    chn = chnn;
+    buf ^= 1;
   }
 }
 
