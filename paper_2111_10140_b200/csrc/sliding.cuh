@@ -25,13 +25,18 @@
 
 namespace afs {
 
+#ifndef AFS_TEAM3
+#define AFS_TEAM3 32   // lanes per run for 3-D windows (power of two, 8..32)
+#endif
+
 template <int D, int MM>
 struct Cfg {
   static constexpr int W = 2 * MM;
   static constexpr int LINES = D == 3 ? W * W : (D == 2 ? W : 1);
-  static constexpr int TEAM =
+  static constexpr int TEAM_AUTO =
       D == 1 ? 1
              : (LINES > 16 ? 32 : (LINES > 8 ? 16 : (LINES > 4 ? 8 : (LINES > 2 ? 4 : (LINES > 1 ? 2 : 1)))));
+  static constexpr int TEAM = (D == 3 && TEAM_AUTO > AFS_TEAM3) ? AFS_TEAM3 : TEAM_AUTO;
   static constexpr int LPL = (LINES + TEAM - 1) / TEAM;
   static constexpr int TPW = 32 / TEAM;
 };

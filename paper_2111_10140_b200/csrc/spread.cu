@@ -109,6 +109,7 @@ int v2_rhs_group(int D, int m, int R) {
   if (D != 1) {
     team = 1;
     while (team < lines && team < 32) team *= 2;
+    if (D == 3 && team > AFS_TEAM3) team = AFS_TEAM3;
   }
   const int lpl = (lines + team - 1) / team;
   if (lpl * W > 64) return 0;
