@@ -331,6 +331,8 @@ class _Plan:
             out = torch.empty((R, self.Nt), dtype=torch.float64, device=self.device)
             self.apply_device(a, out, R)
             return out[0] if one else out.t()
+        if torch.is_tensor(alpha):
+            return self._apply_host_tensor(alpha)
         arr = np.asarray(alpha, dtype=np.float64)
         one = arr.ndim == 1
         if not (arr.ndim in (1, 2) and arr.shape[0] == self.N):
@@ -367,6 +369,40 @@ class _Plan:
                 ev.synchronize()
                 dst[:, lo:hi].copy_(h_out[:, lo:hi])
             return res[0] if one else res.T
+
+    def _apply_host_tensor(self, alpha):
+        """torch CPU tensor in -> torch CPU tensor out.  From pinned memory the H2D copy is
+        one async DMA straight into the device staging buffer (no host staging), and the
+        result comes back into pinned memory."""
+        torch = _torch()
+        if alpha.dim() not in (1, 2) or alpha.shape[0] != self.N:
+            raise ShapeError(f"alpha must have length {self.N}, got {tuple(alpha.shape)}")
+        one = alpha.dim() == 1
+        R = 1 if one else alpha.shape[1]
+        if R > self.max_rhs:
+            raise ShapeError(f"at most {self.max_rhs} right-hand sides per apply")
+        a = alpha.to(torch.float64)
+        pinned = a.is_pinned()
+        with self._lock:
+            key = ("tensor", R)
+            st = self._stage.get(key)
+            if st is None:
+                st = (torch.empty((self.N, R), dtype=torch.float64, device=self.device),
+                      torch.empty((R, self.N), dtype=torch.float64, device=self.device),
+                      torch.empty((R, self.Nt), dtype=torch.float64, device=self.device))
+                self._stage[key] = st
+            d_raw, d_in, d_out = st
+            stream = torch.cuda.current_stream(self.device)
+            if one:
+                d_in[0].copy_(a, non_blocking=pinned)
+            else:   # (N, R) row-major on the host: copy as is, transpose on the device
+                d_raw.copy_(a.contiguous(), non_blocking=pinned)
+                d_in.copy_(d_raw.t())
+            self.apply_device(d_in, d_out, R)
+            res = torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=pinned)
+            res.copy_(d_out, non_blocking=pinned)
+            stream.synchronize()
+            return res[0] if one else res.t()
 
 
 class AnovaKernelOperator:
