@@ -383,7 +383,8 @@ def run_ours(args):
             "updates_per_s": w.N * w.P * value,
             "hbm_fraction_matvec": {"bytes_per_matvec": Btot,
                                     "achieved_gbs": Btot / (ms_step * 1e-3) / 1e9,
-                                    "frac_of_measured": Btot / (ms_step * 1e-3) / 1e9 / peak},
+                                    "frac_of_measured": Btot / (ms_step * 1e-3) / 1e9 / peak,
+                                    "frac_of_8tbs": Btot / (ms_step * 1e-3) / 8e12},
             "stage_ms": stage,
             "roofline": {"bound": "hbm", "kernel": f"{kind} ({d}-D windows)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",

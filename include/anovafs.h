@@ -126,6 +126,19 @@ int afs_plan_grids(afs_plan* plan, double** grids, int64_t* doubles_per_rhs);
  * >= doubles_per_rhs * max_rhs; the plan stops using (and frees) its own buffer. */
 int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles);
 
+/* Split spectral stage for point sharding with a spectrum exchange:
+ * afs_spectral_forward turns every window's grid into its pruned spectrum E (.) F(g) --
+ * complex, laid out like the window's multiplier ([j0][j1][k], K^(d-1)*(M/2+1) entries) --
+ * in the plan's spectrum buffer (afs_plan_spectra: base pointer as doubles, doubles per rhs =
+ * 2 * sum of multiplier lengths); the caller may all-reduce it across ranks (the spread and
+ * the transform are linear in the nodes); afs_spectral_inverse turns it back into grids
+ * for afs_gather.  forward + inverse == afs_spectral up to rounding. */
+int afs_spectral_forward(afs_plan* plan, int32_t nrhs, void* stream);
+int afs_spectral_inverse(afs_plan* plan, int32_t nrhs, void* stream);
+int afs_plan_spectra(afs_plan* plan, double** spectra, int64_t* doubles_per_rhs);
+/* caller-owned spectrum buffer (16-byte aligned, >= doubles_per_rhs * max_rhs doubles) */
+int afs_plan_bind_spectra(afs_plan* plan, double* buffer, int64_t capacity_doubles);
+
 /* Stage profiling: when enabled, every afs_apply records CUDA events around
  * its spread / spectral / gather stages on the caller's stream, waits for them
  * and accumulates the device milliseconds (this adds one stream sync per

@@ -84,6 +84,9 @@ struct afs_plan {
   double* grids = nullptr;          // [rhs][sum of cells]  (rhs-major)
   bool grids_owned = true;          // false after afs_plan_bind_grids
   int64_t grid_total = 0;           // sum of cells over windows
+  double2* spec = nullptr;          // [rhs][spec_total] pruned spectra (split spectral stage)
+  bool spec_owned = true;           // false after afs_plan_bind_spectra
+  int64_t spec_total = 0;           // complex entries per rhs (= sum of multiplier lengths)
   double2* scratch_a = nullptr;
   double2* scratch_b = nullptr;
   int64_t scratch_a_len = 0, scratch_b_len = 0;   // complex entries per rhs
@@ -114,7 +117,7 @@ namespace afs {
 
 // stages (implemented in spread.cu / spectral.cu / gather.cu / cg.cu)
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s);
-void spectral_all(afs_plan* p, int R, cudaStream_t s);
+void spectral_all(afs_plan* p, int R, cudaStream_t s, int mode = 0);   // 0 fused, 1 fwd, 2 inv
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
 void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
                 int R, cudaStream_t s);

@@ -158,6 +158,7 @@ static void free_plan(afs_plan* p) {
   cudaFree(p->mult);
   cudaFree(p->twiddle);
   if (p->grids_owned) cudaFree(p->grids);
+  if (p->spec_owned) cudaFree(p->spec);
   cudaFree(p->scratch_a);
   cudaFree(p->scratch_b);
   cudaFree(p->cg.r);
@@ -255,6 +256,7 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       launches += 1 + (w.d == 1 ? 1 : (w.d == 2 ? 3 : 5));
     }
     p->grid_total = grid_total;
+    p->spec_total = mult_total;   // one pruned spectrum per window, laid out like E
     p->launches_per_apply = launches;
 
     const size_t src_bytes = sizeof(double) * p->Ns * p->dtot;
@@ -365,6 +367,60 @@ int afs_spectral(afs_plan* plan, int32_t nrhs, void* stream) {
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
     afs::spectral_all(plan, nrhs, (cudaStream_t)stream);
+  });
+}
+
+static void ensure_spectra(afs_plan* plan) {
+  if (plan->spec) return;
+  const size_t bytes = sizeof(double2) * (size_t)plan->spec_total * plan->max_rhs;
+  AFS_CUDA(cudaMalloc(&plan->spec, bytes));
+  plan->spec_owned = true;
+  plan->device_bytes += (int64_t)bytes;
+}
+
+int afs_spectral_forward(afs_plan* plan, int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    check_rhs(plan, nrhs);
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    ensure_spectra(plan);
+    afs::spectral_all(plan, nrhs, (cudaStream_t)stream, 1);
+  });
+}
+
+int afs_spectral_inverse(afs_plan* plan, int32_t nrhs, void* stream) {
+  return afs::guarded([&] {
+    check_rhs(plan, nrhs);
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    if (!plan->spec) throw afs::Error(AFS_ERR_VALIDATION, "afs_spectral_inverse before forward");
+    afs::spectral_all(plan, nrhs, (cudaStream_t)stream, 2);
+  });
+}
+
+int afs_plan_spectra(afs_plan* plan, double** spectra, int64_t* doubles_per_rhs) {
+  return afs::guarded([&] {
+    if (!plan || !spectra || !doubles_per_rhs) throw afs::Error(AFS_ERR_VALIDATION, "null argument");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    ensure_spectra(plan);
+    *spectra = reinterpret_cast<double*>(plan->spec);
+    *doubles_per_rhs = 2 * plan->spec_total;
+  });
+}
+
+int afs_plan_bind_spectra(afs_plan* plan, double* buffer, int64_t capacity_doubles) {
+  return afs::guarded([&] {
+    if (!plan || !buffer) throw afs::Error(AFS_ERR_VALIDATION, "null plan/buffer");
+    if (capacity_doubles < 2 * plan->spec_total * plan->max_rhs)
+      throw afs::Error(AFS_ERR_SHAPE, "spectrum buffer smaller than doubles_per_rhs * max_rhs");
+    if (reinterpret_cast<uintptr_t>(buffer) % 16 != 0)
+      throw afs::Error(AFS_ERR_VALIDATION, "spectrum buffer must be 16-byte aligned");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    if (plan->spec_owned && plan->spec) cudaFree(plan->spec);
+    plan->spec = reinterpret_cast<double2*>(buffer);
+    plan->spec_owned = false;
   });
 }
 

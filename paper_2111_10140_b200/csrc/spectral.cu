@@ -42,6 +42,9 @@ struct LinePass {
   // four-step kernel only: 1 = pairs of full real lines in (last-axis forward), 2 = pairs of
   // half spectra in, full real lines out (last-axis inverse); the generic kernel ignores it
   int pack;
+  // multiply stored element e of line q by mult[q + e*inner] (forward half of the split
+  // spectral stage: the kept bins leave the pass already multiplied by E)
+  int mult_out;
   const void* in;
   void* out;
   const double* mult;
@@ -230,7 +233,11 @@ __global__ void __launch_bounds__(256) k_line_pass(const LinePass p, const Batch
       const int64_t base = s_outb[li];
       if (base < 0) continue;
       const int64_t a = base + e * p.out_e;
-      const double2 v = R[li * ls + bin_of(e, p.out_sym, p.half, n)];
+      double2 v = R[li * ls + bin_of(e, p.out_sym, p.half, n)];
+      if (p.mult_out) {
+        const double m = mult[s_q[li] + (int64_t)e * p.inner];
+        v = make_double2(v.x * m, v.y * m);
+      }
       if (p.out_real)
         ((double*)p.out)[a] = v.x;
       else
@@ -538,7 +545,11 @@ __global__ void __launch_bounds__(128, (N1 * N2 >= 512) ? 2 : 4) k_line_pass_4s(
       const int64_t a = base + e * p.out_e;
       const int k = bin_of(e, p.out_sym, p.half, n);
       const int pos = fused ? (k % N2) * (N1 + 1) + k / N2 : (k % N1) * (N2 + 1) + k / N1;
-      const double2 v = S[li * ls + pos];
+      double2 v = S[li * ls + pos];
+      if (p.mult_out) {
+        const double m = mult[s_q[li] + (int64_t)e * p.inner];
+        v = make_double2(v.x * m, v.y * m);
+      }
       if (p.out_real)
         ((double*)p.out)[a] = v.x;
       else
@@ -606,34 +617,55 @@ static void run_pass(afs_plan* pl, LinePass p, const BatchOff& off, int nb, cuda
   k_line_pass<<<grid, lpc * T, smem, s>>>(p, off, pl->twiddle, lpc, T);
 }
 
-void spectral_all(afs_plan* pl, int R, cudaStream_t s) {
+// mode 0: grid -> grid (fused first-axis pass).  mode 1: grid -> pruned spectrum E (.) F(g)
+// in pl->spec (layout of the multiplier, complex).  mode 2: pruned spectrum -> grid.
+// Modes 1 + 2 split the stage so point-sharded ranks can all-reduce the spectrum (linear in
+// the nodes) instead of the oversampled grid: K^(d-1)*(M/2+1) instead of n^d values.
+void spectral_all(afs_plan* pl, int R, cudaStream_t s, int mode) {
   const int n = pl->n, M = pl->M, H = pl->H, K = M + 1;
   const int64_t gs = pl->grid_total;
+  const int64_t ss = pl->spec_total;
   for (int d = 1; d <= 3; ++d) {
     std::vector<int> ws;
     for (int l = 0; l < pl->P; ++l)
       if (pl->win[l].d == d) ws.push_back(l);
     for (size_t b0 = 0; b0 < ws.size(); b0 += kMaxBatch) {
       const int nb = (int)std::min<size_t>(kMaxBatch, ws.size() - b0);
-      BatchOff grid_off{}, a_off{}, b_off{}, m_off{}, none{};
+      BatchOff grid_off{}, a_off{}, b_off{}, m_off{}, s_off{};
       for (int i = 0; i < nb; ++i) {
         const Window& w = pl->win[ws[b0 + i]];
         grid_off.in[i] = grid_off.out[i] = w.grid_off;
         a_off.in[i] = a_off.out[i] = w.scratch_a_off;
         b_off.in[i] = b_off.out[i] = w.scratch_b_off;
         m_off.mult[i] = w.mult_off;
+        s_off.in[i] = s_off.out[i] = w.mult_off;   // spectrum shares the multiplier layout
       }
       double* g = pl->grids;
       LinePass p{};
       if (d == 1) {
-        // single fused pass: real line -> keep k in 0..M/2 -> * E -> inverse -> real
         BatchOff o = grid_off;
         for (int i = 0; i < nb; ++i) o.mult[i] = m_off.mult[i];
         p.nlines = R; p.inner = 1;
-        p.in_o = gs; p.in_q = 0; p.in_e = 1; p.in_count = n; p.in_real = 1;
-        p.out_o = gs; p.out_q = 0; p.out_e = 1; p.out_count = n; p.out_real = 1;
-        p.dir = -1; p.has_mult = 1; p.mult = pl->mult; p.keep_count = H; p.keep_sym = 0;
-        p.in = g; p.out = g;
+        p.mult = pl->mult;
+        if (mode == 0) {
+          // single fused pass: real line -> keep k in 0..M/2 -> * E -> inverse -> real
+          p.in_o = gs; p.in_q = 0; p.in_e = 1; p.in_count = n; p.in_real = 1;
+          p.out_o = gs; p.out_q = 0; p.out_e = 1; p.out_count = n; p.out_real = 1;
+          p.dir = -1; p.has_mult = 1; p.keep_count = H; p.keep_sym = 0;
+          p.in = g; p.out = g;
+        } else if (mode == 1) {
+          for (int i = 0; i < nb; ++i) o.out[i] = s_off.out[i];
+          p.in_o = gs; p.in_q = 0; p.in_e = 1; p.in_count = n; p.in_real = 1;
+          p.out_o = ss; p.out_q = 0; p.out_e = 1; p.out_count = H;
+          p.dir = -1; p.mult_out = 1;
+          p.in = g; p.out = pl->spec;
+        } else {
+          for (int i = 0; i < nb; ++i) o.in[i] = s_off.in[i];
+          p.in_o = ss; p.in_q = 0; p.in_e = 1; p.in_count = H;
+          p.out_o = gs; p.out_q = 0; p.out_e = 1; p.out_count = n; p.out_real = 1;
+          p.dir = +1;
+          p.in = pl->spec; p.out = g;
+        }
         run_pass(pl, p, o, nb, s);
         continue;
       }
@@ -642,43 +674,70 @@ void spectral_all(afs_plan* pl, int R, cudaStream_t s) {
       const int64_t n0 = n;
       const int64_t rows = (d == 3) ? (int64_t)n * n : (int64_t)n;   // last-axis lines per rhs
       const int64_t aper = rows * H;                                  // A per rhs
-      // pass 1: real last axis -> half spectrum (k in 0..M/2):  g -> A[r][rows][H]
-      BatchOff o1{};
-      for (int i = 0; i < nb; ++i) { o1.in[i] = grid_off.in[i]; o1.out[i] = a_off.out[i]; }
-      p = LinePass{};
-      p.nlines = R * rows; p.inner = rows;
-      p.in_o = gs; p.in_q = n; p.in_e = 1; p.in_count = n; p.in_real = 1;
-      p.out_o = aper; p.out_q = H; p.out_e = 1; p.out_count = H;
-      p.dir = -1; p.in = g; p.out = A; p.mult = pl->mult;
-      p.pack = 1;
-      run_pass(pl, p, o1, nb, s);
-      double2* F = A;
-      BatchOff fo = a_off;
-      int64_t fq = H;   // first-axis lines per rhs (inner)
-      if (d == 3) {
-        // middle axis forward, keep j in 0..M:  A[r][i0][i1][k] -> B[r][i0][j1][k]
-        BatchOff o2{};
-        for (int i = 0; i < nb; ++i) { o2.in[i] = a_off.in[i]; o2.out[i] = b_off.out[i]; }
+      // first-axis lines live in F = A (d=2) or B (d=3); fq lines per rhs
+      double2* F = d == 3 ? B : A;
+      const BatchOff fo = d == 3 ? b_off : a_off;
+      const int64_t fq = d == 3 ? (int64_t)K * H : (int64_t)H;
+      if (mode != 2) {
+        // pass 1: real last axis -> half spectrum (k in 0..M/2):  g -> A[r][rows][H]
+        BatchOff o1{};
+        for (int i = 0; i < nb; ++i) { o1.in[i] = grid_off.in[i]; o1.out[i] = a_off.out[i]; }
         p = LinePass{};
-        p.nlines = R * n0 * H; p.inner = H;
-        p.in_o = (int64_t)n * H; p.in_q = 1; p.in_e = H; p.in_count = n;
-        p.out_o = (int64_t)K * H; p.out_q = 1; p.out_e = H; p.out_count = K; p.out_sym = 1;
-        p.dir = -1; p.in = A; p.out = B; p.mult = pl->mult;
-        run_pass(pl, p, o2, nb, s);
-        F = B;
-        fo = b_off;
-        fq = (int64_t)K * H;
+        p.nlines = R * rows; p.inner = rows;
+        p.in_o = gs; p.in_q = n; p.in_e = 1; p.in_count = n; p.in_real = 1;
+        p.out_o = aper; p.out_q = H; p.out_e = 1; p.out_count = H;
+        p.dir = -1; p.in = g; p.out = A; p.mult = pl->mult;
+        p.pack = 1;
+        run_pass(pl, p, o1, nb, s);
+        if (d == 3) {
+          // middle axis forward, keep j in 0..M:  A[r][i0][i1][k] -> B[r][i0][j1][k]
+          BatchOff o2{};
+          for (int i = 0; i < nb; ++i) { o2.in[i] = a_off.in[i]; o2.out[i] = b_off.out[i]; }
+          p = LinePass{};
+          p.nlines = R * n0 * H; p.inner = H;
+          p.in_o = (int64_t)n * H; p.in_q = 1; p.in_e = H; p.in_count = n;
+          p.out_o = (int64_t)K * H; p.out_q = 1; p.out_e = H; p.out_count = K; p.out_sym = 1;
+          p.dir = -1; p.in = A; p.out = B; p.mult = pl->mult;
+          run_pass(pl, p, o2, nb, s);
+        }
       }
-      // fused first-axis pass: forward, keep j0 in 0..M, * E, inverse (in place)
-      BatchOff o3 = fo;
-      for (int i = 0; i < nb; ++i) o3.mult[i] = m_off.mult[i];
-      p = LinePass{};
-      p.nlines = R * fq; p.inner = fq;
-      p.in_o = n0 * fq; p.in_q = 1; p.in_e = fq; p.in_count = n;
-      p.out_o = n0 * fq; p.out_q = 1; p.out_e = fq; p.out_count = n;
-      p.dir = -1; p.has_mult = 1; p.mult = pl->mult; p.keep_count = K; p.keep_sym = 1;
-      p.in = F; p.out = F;
-      run_pass(pl, p, o3, nb, s);
+      if (mode == 0) {
+        // fused first-axis pass: forward, keep j0 in 0..M, * E, inverse (in place)
+        BatchOff o3 = fo;
+        for (int i = 0; i < nb; ++i) o3.mult[i] = m_off.mult[i];
+        p = LinePass{};
+        p.nlines = R * fq; p.inner = fq;
+        p.in_o = n0 * fq; p.in_q = 1; p.in_e = fq; p.in_count = n;
+        p.out_o = n0 * fq; p.out_q = 1; p.out_e = fq; p.out_count = n;
+        p.dir = -1; p.has_mult = 1; p.mult = pl->mult; p.keep_count = K; p.keep_sym = 1;
+        p.in = F; p.out = F;
+        run_pass(pl, p, o3, nb, s);
+      } else if (mode == 1) {
+        // first axis forward, keep j0 in 0..M, * E -> spectrum [j0][q]
+        BatchOff o3{};
+        for (int i = 0; i < nb; ++i) {
+          o3.in[i] = fo.in[i]; o3.out[i] = s_off.out[i]; o3.mult[i] = m_off.mult[i];
+        }
+        p = LinePass{};
+        p.nlines = R * fq; p.inner = fq;
+        p.in_o = n0 * fq; p.in_q = 1; p.in_e = fq; p.in_count = n;
+        p.out_o = ss; p.out_q = 1; p.out_e = fq; p.out_count = K; p.out_sym = 1;
+        p.dir = -1; p.mult_out = 1; p.mult = pl->mult;
+        p.in = F; p.out = pl->spec;
+        run_pass(pl, p, o3, nb, s);
+        continue;
+      } else {
+        // spectrum [j0][q] -> first axis inverse (n values) in F
+        BatchOff o3{};
+        for (int i = 0; i < nb; ++i) { o3.in[i] = s_off.in[i]; o3.out[i] = fo.out[i]; }
+        p = LinePass{};
+        p.nlines = R * fq; p.inner = fq;
+        p.in_o = ss; p.in_q = 1; p.in_e = fq; p.in_count = K; p.in_sym = 1;
+        p.out_o = n0 * fq; p.out_q = 1; p.out_e = fq; p.out_count = n;
+        p.dir = +1; p.mult = pl->mult;
+        p.in = pl->spec; p.out = F;
+        run_pass(pl, p, o3, nb, s);
+      }
       if (d == 3) {
         // middle axis inverse: B[r][i0][j1][k] -> A[r][i0][i1][k]
         BatchOff o4{};
@@ -700,7 +759,6 @@ void spectral_all(afs_plan* pl, int R, cudaStream_t s) {
       p.dir = +1; p.in = A; p.out = g; p.mult = pl->mult;
       p.pack = (2 * (H - 1) < n) ? 2 : 0;   // Hermitian completion needs k and -k distinct
       run_pass(pl, p, o5, nb, s);
-      (void)none;
     }
   }
   AFS_CUDA(cudaGetLastError());

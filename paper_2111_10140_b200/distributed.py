@@ -138,10 +138,15 @@ class PointSharded:
 
 
 class CudaPointBackend:
-    """Stage backend over a CUDA plan whose grid buffer is a torch tensor (NCCL-visible)."""
+    """Stage backend over a CUDA plan whose exchange buffer is a torch tensor (NCCL-visible).
+
+    exchange="spectrum" (default): spread + forward transform locally, all-reduce
+    the pruned spectra E (.) F(g) -- K^(d-1)(M/2+1) complex values per window, 17 MB per rhs
+    for C4 -- then inverse transform + gather.  exchange="grid": all-reduce the real
+    oversampled grids (n^d values, 134 MB per rhs for C4) and run the fused spectral stage."""
 
     def __init__(self, X_local, windows, sigma, *, M, m, oversampling=2.0, weights=None,
-                 max_rhs=1, group=None, device=None):
+                 max_rhs=1, group=None, device=None, exchange="spectrum"):
         import torch
 
         from .operators import AnovaKernelOperator, bbox_scaling
@@ -155,20 +160,35 @@ class CudaPointBackend:
                                       weights=weights if weights is not None else [1.0 / P] * P,
                                       device=device, max_rhs=max_rhs, scaling=scaling)
         self.plan = self.op._plan
-        per = self.plan.grid_doubles_per_rhs()
-        self.grids = torch.zeros(per * self.plan.max_rhs, dtype=torch.float64,
-                                 device=self.plan.device)
-        self.plan.bind_grids(self.grids)
+        if exchange not in ("spectrum", "grid"):
+            raise ValueError(f"exchange must be 'spectrum' or 'grid', got {exchange!r}")
+        self.exchange = exchange
+        if exchange == "grid":
+            self.per = self.plan.grid_doubles_per_rhs()
+            self.buf = torch.zeros(self.per * self.plan.max_rhs, dtype=torch.float64,
+                                   device=self.plan.device)
+            self.plan.bind_grids(self.buf)
+        else:
+            self.per = self.plan.spectrum_doubles_per_rhs()
+            self.buf = torch.zeros(self.per * self.plan.max_rhs, dtype=torch.float64,
+                                   device=self.plan.device)
+            self.plan.bind_spectra(self.buf)
         self.R = 1
 
     def spread(self, alpha):
+        """Local spread (+ forward transform): returns the buffer to all-reduce."""
         a = alpha if alpha.dim() == 2 else alpha[None, :]
         self.R = a.shape[0]
         self.plan.spread_device(a.contiguous(), self.R)
-        return self.grids[: self.plan.grid_doubles_per_rhs() * self.R]
+        if self.exchange == "spectrum":
+            self.plan.spectral_forward_device(self.R)
+        return self.buf[: self.per * self.R]
 
-    def spectral(self, grids):
-        self.plan.spectral_device(self.R)
+    def spectral(self, exchanged):
+        if self.exchange == "spectrum":
+            self.plan.spectral_inverse_device(self.R)
+        else:
+            self.plan.spectral_device(self.R)
 
     def gather(self, grids):
         import torch

@@ -294,6 +294,27 @@ class _Plan:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         _native.check(self.lib.afs_spectral(self.handle, int(nrhs), stream))
 
+    def spectrum_doubles_per_rhs(self):
+        ptr = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _native.check(self.lib.afs_plan_spectra(self.handle, ctypes.byref(ptr), ctypes.byref(n)))
+        return int(n.value)
+
+    def bind_spectra(self, buf):
+        """Make the split spectral stage use `buf` (cuda float64, >= per_rhs*max_rhs)."""
+        _native.check(self.lib.afs_plan_bind_spectra(self.handle, buf.data_ptr(), buf.numel()))
+        self._bound_spectra = buf   # keep alive
+
+    def spectral_forward_device(self, nrhs):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.afs_spectral_forward(self.handle, int(nrhs), stream))
+
+    def spectral_inverse_device(self, nrhs):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.afs_spectral_inverse(self.handle, int(nrhs), stream))
+
     def gather_device(self, out, nrhs):
         torch = _torch()
         stream = torch.cuda.current_stream(self.device).cuda_stream

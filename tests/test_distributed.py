@@ -92,7 +92,7 @@ def test_window_sharded_matches_single_process(tmp_path):
 class NumpyPointBackend:
     """numpy model of the device stages for one window (spread / spectral / gather)."""
 
-    def __init__(self, X_local, win, sigma, M, m, group=None):
+    def __init__(self, X_local, win, sigma, M, m, group=None, exchange="grid"):
         from oracle import fastsum_oracle as orc
         from paper_2111_10140_b200 import GaussianKernel, PeriodizationConfig, regularize_kernel
         from paper_2111_10140_b200.distributed import global_bbox
@@ -100,6 +100,7 @@ class NumpyPointBackend:
         from paper_2111_10140_b200.spectrum import window_multiplier
 
         self.orc = orc
+        self.exchange = exchange
         cfg = PeriodizationConfig(coeff_grid=M)
         (lo, hi), = global_bbox(X_local, [win], group)
         center, scale = bbox_scaling(lo, hi, cfg)
@@ -127,55 +128,77 @@ class NumpyPointBackend:
         return flat, w
 
     def spread(self, alpha):
+        """Local spread; with exchange="spectrum" also the forward half of the spectral stage,
+        so the returned buffer (what PointSharded all-reduces) is the pruned spectrum."""
         flat, w = self._tensor()
         g = np.bincount(flat.ravel(), (alpha.numpy()[:, None] * w).ravel(), minlength=self.n ** self.d)
-        self.grids = torch.from_numpy(g)
-        return self.grids
+        if self.exchange == "grid":
+            self.buf = torch.from_numpy(g)
+        else:
+            S = self._forward(g)
+            self.shape = S.shape
+            self.buf = torch.from_numpy(np.ascontiguousarray(S).view(np.float64).ravel().copy())
+        return self.buf
 
-    def spectral(self, grids):
+    def _forward(self, g):
         n, M, d = self.n, self.M, self.d
         H = M // 2 + 1
-        g = grids.numpy().reshape((n,) * d)
         sym = (np.arange(M + 1) - M // 2) % n
-        A = np.fft.fft(g, axis=-1)[..., :H]
+        A = np.fft.fft(g.reshape((n,) * d), axis=-1)[..., :H]
         if d == 3:
             A = np.fft.fft(A, axis=1)[:, sym, :]
         if d >= 2:
-            F = np.fft.fft(A, axis=0)
-            Y = np.zeros_like(F)
-            Y[sym] = F[sym] * self.E
+            A = np.fft.fft(A, axis=0)[sym]
+        return A * self.E
+
+    def _inverse(self, S):
+        n, M, d = self.n, self.M, self.d
+        H = M // 2 + 1
+        sym = (np.arange(M + 1) - M // 2) % n
+        A = S
+        if d >= 2:
+            Y = np.zeros((n,) + S.shape[1:], dtype=complex)
+            Y[sym] = S
             A = n * np.fft.ifft(Y, axis=0)
-        else:
-            A = A * self.E
         if d == 3:
             full = np.zeros((n, n, H), dtype=complex)
             full[:, sym, :] = A
             A = n * np.fft.ifft(full, axis=1)
         line = np.zeros(A.shape[:-1] + (n,), dtype=complex)
         line[..., :H] = A
-        grids.copy_(torch.from_numpy((n * np.fft.ifft(line, axis=-1)).real.ravel()))
+        return (n * np.fft.ifft(line, axis=-1)).real.ravel()
 
-    def gather(self, grids):
+    def spectral(self, buf):
+        if self.exchange == "grid":
+            self.grid = self._inverse(self._forward(buf.numpy()))
+        else:
+            self.grid = self._inverse(buf.numpy().view(np.complex128).reshape(self.shape))
+
+    def gather(self, buf):
         flat, w = self._tensor()
-        return torch.from_numpy((grids.numpy()[flat] * w).sum(1))
+        return torch.from_numpy((self.grid[flat] * w).sum(1))
 
 
 def _point_worker(rank, world, port, out_path):
     _init(rank, world, port)
     from paper_2111_10140_b200.distributed import PointSharded
 
+    exchange = out_path.rsplit("_", 1)[-1]
     wl = synthetic.c4(N=600, R=1)
     shard = np.array_split(np.arange(wl.N), world)[rank]
-    be = NumpyPointBackend(wl.X[shard], (0, 1, 2), wl.sigma, wl.M, wl.m)
+    be = NumpyPointBackend(wl.X[shard], (0, 1, 2), wl.sigma, wl.M, wl.m, exchange=exchange)
     res = PointSharded(be).apply(torch.from_numpy(wl.alpha[shard, 0].copy())).numpy()
     np.save(out_path + f".{rank}.npy", res)
     dist.destroy_process_group()
 
 
-def test_point_sharded_matches_single_process(tmp_path):
+@pytest.mark.parametrize("exchange", ["grid", "spectrum"])
+def test_point_sharded_matches_single_process(tmp_path, exchange):
+    """world 2 over gloo: all-reducing either the grids or the pruned spectra (linear in the
+    node set) reproduces the single-process fast sum."""
     from oracle import fastsum_oracle as orc
 
-    out = str(tmp_path / "ps")
+    out = str(tmp_path / f"ps_{exchange}")
     _run(_point_worker, 2, out)
     wl = synthetic.c4(N=600, R=1)
     ref = orc.fastsum_apply(wl.X, wl.alpha[:, 0], wl.sigma, wl.M, wl.m)
