@@ -353,7 +353,9 @@ def run_ours(args):
     n = plan.n
     dom_bytes = w.N * 8 * d + w.N * 8 + 8 * n ** d      # coordinates + alpha/out + grid
     achieved = dom_bytes / t_launch / 1e9
-    fma_per_node = (2 * w.m) ** d + 2 * w.m * d * 13 + (2 * w.m) ** (d - 1)   # touches + Horner
+    # Horner degree of the compile-time window table (kb_tables.inc kb_terms - 1; n = 2M)
+    deg = {1: 13, 2: 12, 3: 12}.get(w.m, 11) if plan.n == 2 * w.M else 13
+    fma_per_node = (2 * w.m) ** d + 2 * w.m * d * deg + (2 * w.m) ** (d - 1)   # touches + Horner
     fp64_tflops = 2.0 * fma_per_node * w.N / t_launch / 1e12
     fp64_peak, fp64_src = measured_fp64_peak()
     traffic = ncu_traffic(f"{kind}_d{d}")

@@ -56,9 +56,10 @@ __device__ __forceinline__ void poly_weights(double f, const PolyTable& T, doubl
   const double x = (refl ? __dsub_rn(1.0, f) : f) - 0.25;
 #pragma unroll
   for (int i = 0; i < 2 * MM; ++i) {
-    double v = TAB == 0 ? T.c[i][kPolyTerms - 1] : kb_coef<TAB, MM>(i, kPolyTerms - 1);
+    constexpr int NT = TAB == 0 ? kPolyTerms : kb_terms<TAB, MM>();
+    double v = TAB == 0 ? T.c[i][NT - 1] : kb_coef<TAB, MM>(i, NT - 1);
 #pragma unroll
-    for (int k = kPolyTerms - 2; k >= 0; --k)
+    for (int k = NT - 2; k >= 0; --k)
       v = fma(v, x, TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k));
     w[i] = v;
   }

@@ -225,8 +225,9 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
   // all W*P*D Horner chains advance together (k outer): W*P*D independent FMAs per step
   // hide the DFMA latency, and each coefficient is materialised once for P*D uses
   double v[W][P][D];
+  constexpr int NT = TAB == 0 ? kPolyTerms : kb_terms<TAB, MM>();   // per-table degree
 #pragma unroll
-  for (int k = kPolyTerms - 1; k >= 0; --k) {
+  for (int k = NT - 1; k >= 0; --k) {
 #pragma unroll
     for (int i = 0; i < W; ++i) {
       const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
@@ -234,7 +235,7 @@ __device__ __forceinline__ void stage_nodes(const NodeIn<D> (&in)[P], const bool
       for (int p = 0; p < P; ++p)
 #pragma unroll
         for (int t = 0; t < D; ++t)
-          v[i][p][t] = k == kPolyTerms - 1 ? c : fma(v[i][p][t], x[p][t], c);
+          v[i][p][t] = k == NT - 1 ? c : fma(v[i][p][t], x[p][t], c);
     }
   }
   // stores are unconditional (rows of dead nodes are never read)

@@ -45,13 +45,14 @@ __device__ __forceinline__ void solo_weights(const double (&nx)[D], const PolyTa
     if (t == D - 1) u_last = wrap_cell((int)fl, n);
   }
   double v[W][D];
+  constexpr int NT = TAB == 0 ? kPolyTerms : kb_terms<TAB, MM>();   // per-table degree
 #pragma unroll
-  for (int k = kPolyTerms - 1; k >= 0; --k) {
+  for (int k = NT - 1; k >= 0; --k) {
 #pragma unroll
     for (int i = 0; i < W; ++i) {
       const double c = TAB == 0 ? T.c[i][k] : kb_coef<TAB, MM>(i, k);
 #pragma unroll
-      for (int t = 0; t < D; ++t) v[i][t] = k == kPolyTerms - 1 ? c : fma(v[i][t], x[t], c);
+      for (int t = 0; t < D; ++t) v[i][t] = k == NT - 1 ? c : fma(v[i][t], x[t], c);
     }
   }
 #pragma unroll
