@@ -160,7 +160,7 @@ class _Plan:
     """Owns one native plan (afs_plan*) and its staging buffers."""
 
     def __init__(self, X, Z, feats, weights, kernel, config, profile, device, max_rhs,
-                 window_eval="poly", scaling=None):
+                 window_eval="poly", scaling=None, multipliers=None):
         torch = _torch()
         self.lib = _native.load()
         self.device = torch.device("cuda", device if device is not None else torch.cuda.current_device())
@@ -176,6 +176,7 @@ class _Plan:
         self.max_rhs = int(max_rhs)
         self.windows = []
         descs = (_native.WindowDesc * len(feats))()
+        self.n_windows = len(feats)
         self._keep = []
         for l, (w, eta) in enumerate(zip(feats, weights)):
             if scaling is not None:
@@ -187,11 +188,16 @@ class _Plan:
                     zlo, zhi = _columns_minmax(Z, w)
                     lo, hi = np.minimum(lo, zlo), np.maximum(hi, zhi)
                 center, scale = bbox_scaling(lo, hi, config)
-            coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w))
-            mult = window_multiplier(coeffs, M, n, m)
+            if multipliers is not None:
+                # caller-supplied spectral multiplier (e.g. the bare NFFT: deconvolution only)
+                coeffs = None
+                mult = np.ascontiguousarray(multipliers[l], dtype=np.float64)
+            else:
+                coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w))
+                mult = window_multiplier(coeffs, M, n, m)
+                self.windows.append(WindowOperator(w, kernel, config, profile, center, scale,
+                                                   coeffs, self.N, self.Nt))
             self._keep.append(mult)
-            self.windows.append(WindowOperator(w, kernel, config, profile, center, scale, coeffs,
-                                               self.N, self.Nt))
             dsc = descs[l]
             dsc.dims = len(w)
             for t in range(len(w)):
@@ -246,7 +252,7 @@ class _Plan:
 
     def window_times(self, reset: bool = True):
         """Per-window (spread_ms, gather_ms) lists accumulated over profiled applies."""
-        P = len(self.windows)
+        P = self.n_windows
         sp = (ctypes.c_double * P)()
         ga = (ctypes.c_double * P)()
         _native.check(self.lib.afs_plan_window_times(self.handle, sp, ga, 1 if reset else 0))
