@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-n", type=int, default=50_000, help="CPU baseline sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bit-reproducible fixed-point spread (afs_plan_set_deterministic)")
     return ap.parse_args()
 
 
@@ -256,7 +258,7 @@ def run_ours(args):
     my_windows = [w.windows[i] for i in mine]
     op = afs.AnovaKernelOperator(w.X, my_windows, w.sigma, afs.AccuracyProfile("c3", 2.0, w.m),
                                  None, afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
-                                 weights=[1.0 / w.P] * len(mine))
+                                 weights=[1.0 / w.P] * len(mine), deterministic=args.deterministic)
     plan = op._plan
     alpha_host = w.alpha
     alpha = torch.from_numpy(alpha_host).to(dev)[None, :].contiguous()
@@ -381,7 +383,9 @@ def run_ours(args):
             "dtype": "f64", "data": "synthetic",
             "config": workload_config(w.N, w.P, w.m, w.M, plan.n,
                                       {"parallelism": f"windows dealt by LPT over {world} GPU(s)"
-                                                      + ("; NCCL all-reduce of the N-vector" if world > 1 else "")}),
+                                                      + ("; NCCL all-reduce of the N-vector" if world > 1 else ""),
+                                       "spread_accumulation": "fixed-point limbs (deterministic)"
+                                                              if args.deterministic else "fp64 atomics"}),
             "updates_per_s": w.N * w.P * value,
             "hbm_fraction_matvec": {"bytes_per_matvec": Btot,
                                     "achieved_gbs": Btot / (ms_step * 1e-3) / 1e9,

@@ -151,6 +151,14 @@ int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset);
  * applies; arrays of n_windows). */
 int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, int32_t reset);
 
+/* Deterministic mode: the spread accumulates each grid cell in exact 120-bit fixed point
+ * (three 40-bit limbs, 64-bit integer reductions) instead of fp64 atomics, with the scale
+ * chosen per apply from max|alpha| so no partial sum can overflow; the limbs are converted
+ * back to fp64 once.  afs_apply / afs_cg_solve then return bit-identical results run to run
+ * for the same plan and inputs (the gather, spectral stage and CG reductions are already
+ * fixed-order).  Costs 3x the grid memory for the limbs and ~2 extra passes per apply. */
+int afs_plan_set_deterministic(afs_plan* plan, int32_t enable);
+
 /* Solve (K + beta I) x = b by plain CG from x0 = 0 (krr.py:76-110).
  * Requires n_targets == n_sources (no separate targets).  b, x: device.
  * Returns AFS_ERR_NUMERICAL on breakdown with *iterations = failing iteration. */

@@ -83,6 +83,7 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_int64)]),
     "afs_plan_bind_spectra": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]),
     "afs_plan_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "afs_plan_set_deterministic": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "afs_plan_stage_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                             ctypes.c_int32]),
     "afs_plan_window_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),

@@ -40,6 +40,12 @@ struct Window {
   int64_t mult_len;    // (M+1)^(d-1) * (M/2+1)
   int64_t mult_off;    // offset into plan->mult
   int64_t scratch_a_off, scratch_b_off;   // per-window spectral scratch (double2, x max_rhs)
+  // deterministic mode (afs_plan_set_deterministic): the spread accumulates fixed-point limbs
+  // of the grids with integer reductions instead of fp64 atomics (see grid_add)
+  long long* det_limbs = nullptr;   // [3][det_stride], null: fp64 atomics
+  int64_t det_stride = 0;           // grid_total * max_rhs
+  const double* det_scale = nullptr;   // device [2]: 2^S, 2^-S for the current apply
+  const double* det_base = nullptr;    // plan->grids (limb index = cell pointer - det_base)
 };
 
 struct SortedSide;   // geometry.cuh
@@ -100,6 +106,10 @@ struct afs_plan {
   afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
   bool use_graphs = true;
   int fft_mode = 0;                    // 0 four-step register FFT where n allows, 1 generic line kernel
+  bool deterministic = false;          // fixed-point spread (afs_plan_set_deterministic)
+  long long* det_limbs = nullptr;      // [3][grid_total * max_rhs]
+  double* det_aux = nullptr;           // [0] max|alpha| bits, [1] 2^S, [2] 2^-S
+  double det_log2_bound = 0.0;         // log2(N * max window product) + margin
   std::vector<afs::GraphEntry> graphs;
   cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -124,6 +134,32 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
 void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
                    int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
 void make_twiddles(afs_plan* p);
+
+// ---------------------------------------------------------------------------
+// grid accumulation of the spread
+// ---------------------------------------------------------------------------
+// Default: one fp64 reduction (RED.E.ADD.F64); the summation order, hence the last bits,
+// depend on scheduling.  Deterministic mode: v * 2^S is split exactly into three signed
+// 40-bit limbs (|v 2^S| < 2^119 by the choice of S, afs_det_scale) that are added with
+// 64-bit integer reductions -- associative, so the grid is bit-identical run to run.
+// Each limb stays below 2^63 for up to 2^23 flushes into one cell.
+__device__ __forceinline__ void grid_add(const Window& w, double* cell, double v) {
+  if (w.det_limbs == nullptr) {
+    atomicAdd(cell, v);
+    return;
+  }
+  const int64_t e = cell - w.det_base;
+  const double x = v * __ldg(w.det_scale);
+  const double h = trunc(x * 0x1p-80);
+  const double r1 = fma(-h, 0x1p80, x);      // exact
+  const double m = trunc(r1 * 0x1p-40);
+  const double r2 = fma(-m, 0x1p40, r1);     // exact, |r2| < 2^40
+  const long long l0 = __double2ll_rn(r2), l1 = (long long)m, l2 = (long long)h;
+  unsigned long long* L = reinterpret_cast<unsigned long long*>(w.det_limbs) + e;
+  if (l0) atomicAdd(L, (unsigned long long)l0);
+  if (l1) atomicAdd(L + w.det_stride, (unsigned long long)l1);
+  if (l2) atomicAdd(L + 2 * w.det_stride, (unsigned long long)l2);
+}
 
 // ---------------------------------------------------------------------------
 // device helpers: exact mirror of the reference window arithmetic

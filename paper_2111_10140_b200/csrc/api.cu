@@ -1,4 +1,5 @@
 // C ABI entry points (include/anovafs.h): plan construction, apply, CG.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -159,6 +160,8 @@ static void free_plan(afs_plan* p) {
   cudaFree(p->twiddle);
   if (p->grids_owned) cudaFree(p->grids);
   if (p->spec_owned) cudaFree(p->spec);
+  cudaFree(p->det_limbs);
+  cudaFree(p->det_aux);
   cudaFree(p->scratch_a);
   cudaFree(p->scratch_b);
   cudaFree(p->cg.r);
@@ -257,6 +260,13 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
     }
     p->grid_total = grid_total;
     p->spec_total = mult_total;   // one pruned spectrum per window, laid out like E
+    {   // deterministic-mode bound: N * (peak of the KB window)^d_max
+      int dmax = 1;
+      for (const Window& w : p->win) dmax = std::max(dmax, w.d);
+      const double peak = std::sinh(p->b * p->m) / (3.141592653589793 * p->m);   // phi(0)
+      p->det_log2_bound = std::log2((double)std::max<int64_t>(p->Ns, 1)) +
+                          dmax * std::log2(std::max(peak, 1.0)) + 2.0;
+    }
     p->launches_per_apply = launches;
 
     const size_t src_bytes = sizeof(double) * p->Ns * p->dtot;
@@ -350,6 +360,8 @@ static void check_rhs(const afs_plan* plan, int32_t nrhs) {
   if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
   if (nrhs < 1 || nrhs > plan->max_rhs) throw afs::Error(AFS_ERR_SHAPE, "nrhs must lie in 1..max_rhs");
 }
+
+static void refresh_det_windows(afs_plan* p);
 
 int afs_spread(afs_plan* plan, const double* alpha, int64_t ld_alpha, int32_t nrhs, void* stream) {
   return afs::guarded([&] {
@@ -452,9 +464,35 @@ int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles
     if (plan->grids_owned) cudaFree(plan->grids);
     plan->grids = buffer;
     plan->grids_owned = false;
-    for (afs::GraphEntry& g : plan->graphs)   // captured graphs reference the old buffer
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    plan->graphs.clear();
+    refresh_det_windows(plan);   // also drops captured graphs (they reference the old buffer)
+  });
+}
+
+static void refresh_det_windows(afs_plan* p) {
+  for (afs::Window& w : p->win) {
+    w.det_limbs = p->deterministic ? p->det_limbs : nullptr;
+    w.det_stride = p->grid_total * p->max_rhs;
+    w.det_scale = p->det_aux ? p->det_aux + 1 : nullptr;
+    w.det_base = p->grids;
+  }
+  for (afs::GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  p->graphs.clear();
+}
+
+int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
+  return afs::guarded([&] {
+    if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    AFS_CUDA(cudaSetDevice(plan->device));
+    if (enable && !plan->det_limbs) {
+      const size_t bytes = sizeof(long long) * 3 * (size_t)plan->grid_total * plan->max_rhs;
+      AFS_CUDA(cudaMalloc(&plan->det_limbs, bytes));
+      AFS_CUDA(cudaMalloc(&plan->det_aux, 4 * sizeof(double)));
+      plan->device_bytes += (int64_t)bytes + 4 * (int64_t)sizeof(double);
+    }
+    plan->deterministic = enable != 0;
+    refresh_det_windows(plan);
   });
 }
 

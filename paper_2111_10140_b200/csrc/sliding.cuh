@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Wi
           if (lg[j].valid) {
 #pragma unroll
             for (int r = 0; r < RG; ++r)
-              if (r < nr) atomicAdd(g + r * rhs_stride + lg[j].off + cm, acc[j][k][r]);
+              if (r < nr) grid_add(w, g + r * rhs_stride + lg[j].off + cm, acc[j][k][r]);
           }
 #pragma unroll
           for (int r = 0; r < RG; ++r) acc[j][k][r] = 0.0;

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
     for (int a = 0; a < LINES; ++a) {
 #pragma unroll
       for (int r = 0; r < RG; ++r) {
-        if (r < nr && acc[a][0][r] != 0.0) atomicAdd(g + r * rhs_stride + rowoff[a] + cm, acc[a][0][r]);
+        if (r < nr && acc[a][0][r] != 0.0) grid_add(w, g + r * rhs_stride + rowoff[a] + cm, acc[a][0][r]);
 #pragma unroll
         for (int k = 0; k + 1 < W; ++k) acc[a][k][r] = acc[a][k + 1][r];
         acc[a][W - 1][r] = 0.0;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
       const int k = (idx / RG) % W;
       const int ln = idx / (RG * W);
       if (r < nr && v[e] != 0.0)
-        atomicAdd(g + r * rhs_stride + rowoff_dyn<D, MM>(ch.col, ln, n) + wrap_cell(top - MM + 1 + k, n), v[e]);
+        grid_add(w, g + r * rhs_stride + rowoff_dyn<D, MM>(ch.col, ln, n) + wrap_cell(top - MM + 1 + k, n), v[e]);
     }
   } else {
     if (has) {
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
 #pragma unroll
           for (int r = 0; r < RG; ++r)
             if (r < nr && acc[a][k][r] != 0.0)
-              atomicAdd(g + r * rhs_stride + rowoff[a] + wrap_cell(top - MM + 1 + k, n), acc[a][k][r]);
+              grid_add(w, g + r * rhs_stride + rowoff[a] + wrap_cell(top - MM + 1 + k, n), acc[a][k][r]);
     }
   }
 }

@@ -31,14 +31,14 @@ __global__ void __launch_bounds__(256) k_spread_red(const double* __restrict__ X
     double* g = grid + r * rhs_stride + w.grid_off;
     if (D == 1) {
 #pragma unroll
-      for (int o0 = 0; o0 < 2 * MM; ++o0) atomicAdd(g + ix[0][o0], __dmul_rn(a, wt[0][o0]));
+      for (int o0 = 0; o0 < 2 * MM; ++o0) grid_add(w, g + ix[0][o0], __dmul_rn(a, wt[0][o0]));
     } else if (D == 2) {
 #pragma unroll 1
       for (int o0 = 0; o0 < 2 * MM; ++o0) {
         const int64_t row = (int64_t)ix[0][o0] * n;
 #pragma unroll
         for (int o1 = 0; o1 < 2 * MM; ++o1)
-          atomicAdd(g + row + ix[D - 1][o1], __dmul_rn(a, __dmul_rn(wt[0][o0], wt[D - 1][o1])));
+          grid_add(w, g + row + ix[D - 1][o1], __dmul_rn(a, __dmul_rn(wt[0][o0], wt[D - 1][o1])));
       }
     } else {
 #pragma unroll 1
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) k_spread_red(const double* __restrict__ X
           const double w01 = __dmul_rn(wt[0][o0], wt[1 % D][o1]);
 #pragma unroll
           for (int o2 = 0; o2 < 2 * MM; ++o2)
-            atomicAdd(g + p1 + ix[D - 1][o2], __dmul_rn(a, __dmul_rn(w01, wt[D - 1][o2])));
+            grid_add(w, g + p1 + ix[D - 1][o2], __dmul_rn(a, __dmul_rn(w01, wt[D - 1][o2])));
         }
       }
     }
@@ -117,8 +117,65 @@ int v2_rhs_group(int D, int m, int R) {
   return 1;
 }
 
+// ---- deterministic mode: scale selection and limb -> fp64 conversion -------------------
+__global__ void k_det_absmax(const double* __restrict__ alpha, int64_t lda, int64_t N, int R,
+                             unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  const int64_t tot = N * R;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, j = i - r * N;
+    m = fmax(m, fabs(alpha[r * lda + j]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// S such that N * max|alpha| * max(window product) * 2^S < 2^119: every partial sum of a
+// cell fits the 120-bit limb range (log2_bound = log2(N * max product) + margin)
+__global__ void k_det_scale(double* aux, double log2_bound) {
+  const double A = __longlong_as_double(*reinterpret_cast<const long long*>(aux));
+  int S = 0;
+  if (A > 0.0) {
+    int ea = 0;
+    frexp(A, &ea);                      // A < 2^ea
+    S = 119 - (int)ceil(log2_bound) - ea;
+  }
+  S = max(-1000, min(1000, S));
+  aux[1] = ldexp(1.0, S);
+  aux[2] = ldexp(1.0, -S);
+}
+
+// exact 128-bit sum of the limbs, then one conversion (two roundings at most) and 2^-S
+__global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stride, int64_t count,
+                               const double* __restrict__ aux, double* __restrict__ grids) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const __int128 v = ((__int128)limbs[2 * stride + i] << 80) + ((__int128)limbs[stride + i] << 40) +
+                     (__int128)limbs[i];
+  const bool neg = v < 0;
+  const unsigned __int128 u = (unsigned __int128)(neg ? -v : v);
+  const double mag = __ull2double_rn((unsigned long long)(u >> 64)) * 0x1p64 +
+                     __ull2double_rn((unsigned long long)u);
+  grids[i] = (neg ? -mag : mag) * aux[2];
+}
+
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
-  AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * p->grid_total * R, s));
+  const bool det = p->deterministic && p->det_limbs;
+  const int64_t cells = p->grid_total * R;
+  if (det) {
+    const int64_t stride = p->grid_total * p->max_rhs;
+    for (int k = 0; k < 3; ++k)
+      AFS_CUDA(cudaMemsetAsync(p->det_limbs + k * stride, 0, sizeof(long long) * cells, s));
+    AFS_CUDA(cudaMemsetAsync(p->det_aux, 0, sizeof(double), s));
+    k_det_absmax<<<592, 256, 0, s>>>(alpha, lda, p->Ns, R,
+                                     reinterpret_cast<unsigned long long*>(p->det_aux));
+    k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound);
+  } else {
+    AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * cells, s));
+  }
   const bool timed = p->profiling && !p->wev_spread.empty();
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
@@ -136,6 +193,10 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
     }
   }
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
+  if (det) {
+    k_det_finalize<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
+        p->det_limbs, p->grid_total * p->max_rhs, cells, p->det_aux, p->grids);
+  }
   AFS_CUDA(cudaGetLastError());
 }
 

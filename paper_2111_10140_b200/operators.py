@@ -241,6 +241,10 @@ class _Plan:
         _native.check(self.lib.afs_plan_get_info(self.handle, ctypes.byref(inf)))
         return {k: getattr(inf, k) for k, _ in _native.PlanInfo._fields_}
 
+    def set_deterministic(self, enable: bool):
+        """Bit-reproducible spread (fixed-point grid accumulation; include/anovafs.h)."""
+        _native.check(self.lib.afs_plan_set_deterministic(self.handle, 1 if enable else 0))
+
     def set_profiling(self, enable: bool):
         _native.check(self.lib.afs_plan_set_profiling(self.handle, 1 if enable else 0))
 
@@ -443,7 +447,7 @@ class AnovaKernelOperator:
 
     def __init__(self, X, windows, sigma, profile="default", targets=None, config=None, *,
                  strict=True, weights=None, device=None, max_rhs=1, window_eval="poly",
-                 scaling=None):
+                 scaling=None, deterministic=False):
         X = _as_matrix(X, "sources")
         if strict:
             if not isinstance(windows, WindowSet):
@@ -473,6 +477,8 @@ class AnovaKernelOperator:
         self.n_targets = X.shape[0] if Z is None else Z.shape[0]
         self._plan = _Plan(X, Z, list(windows.windows), list(windows.weights), kernel, config,
                            profile, device, max_rhs, window_eval, scaling)
+        if deterministic:
+            self._plan.set_deterministic(True)
         self.operators = self._plan.windows
 
     def apply(self, alpha):
@@ -496,7 +502,7 @@ class FastsumOperator:
     """
 
     def __init__(self, kernel, config, sources, targets=None, profile="default", *, device=None,
-                 max_rhs=1, window_eval="poly"):
+                 max_rhs=1, window_eval="poly", deterministic=False):
         if not isinstance(kernel, GaussianKernel):
             raise ValidationError("kernel must be a GaussianKernel")
         profile = resolve_profile(profile)
@@ -517,6 +523,8 @@ class FastsumOperator:
         self.dims = d
         self._plan = _Plan(X, Z, [tuple(range(d))], [1.0], kernel, config, profile, device, max_rhs,
                            window_eval)
+        if deterministic:
+            self._plan.set_deterministic(True)
         w = self._plan.windows[0]
         self.scale = w.scale
         self.center = w.center
