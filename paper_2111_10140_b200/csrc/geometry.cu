@@ -63,10 +63,13 @@ static int chunk_cap_for(int d, int64_t N) {
   // d = 3: one 32-lane team per run; d <= 2: one warp per run, 32 nodes per lane.
   // Up to 1024 nodes per run amortise the window flushes; small windows use shorter
   // runs so that a launch still has >= ~8 warps per SM (148 SMs).
-  (void)d;
   int64_t hi = 1024;
   if (const char* e = getenv("AFS_CHUNK_CAP_MAX")) hi = std::max(64, atoi(e)) / 32 * 32;   // tuning hook
-  int64_t cap = N / (148 * 8);
+  // warps per SM the launch should fill: the 1-D kernels hold ~100 registers (24 warps
+  // resident), the 2-D/3-D ones ~230 (8 warps)
+  int per_sm = d == 1 ? 24 : 8;
+  if (const char* e = getenv("AFS_CHUNK_WARPS_1D")) if (d == 1) per_sm = std::max(1, atoi(e));
+  int64_t cap = N / (148 * per_sm);
   cap = (cap + 31) / 32 * 32;
   return (int)std::max<int64_t>(64, std::min<int64_t>(hi, cap));
 }

@@ -252,6 +252,26 @@ __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const 
       if (r < nr && v[e] != 0.0)
         grid_add(w, g + r * rhs_stride + rowoff_dyn<D, MM>(ch.col, ln, n) + wrap_cell(top - MM + 1 + k, n), v[e]);
     }
+  } else if constexpr (TOT < 32) {
+    // small windows (1-D): all-reduce each entry across the warp, lane e flushes entry e
+    // (32 lanes x TOT reductions into the same few cells would serialise in L2)
+#pragma unroll
+    for (int e = 0; e < TOT; ++e) {
+      if (!has) v[e] = 0.0;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) v[e] += __shfl_xor_sync(0xffffffffu, v[e], s);
+    }
+    double mine = 0.0;
+#pragma unroll
+    for (int e = 0; e < TOT; ++e)
+      if (lane == e) mine = v[e];
+    if (lane < TOT) {
+      const int r = lane % RG;
+      const int k = (lane / RG) % W;
+      const int ln = lane / (RG * W);
+      if (r < nr && mine != 0.0)
+        grid_add(w, g + r * rhs_stride + rowoff_dyn<D, MM>(ch.col, ln, n) + wrap_cell(top - MM + 1 + k, n), mine);
+    }
   } else {
     if (has) {
 #pragma unroll
