@@ -81,9 +81,9 @@ typedef struct afs_plan_desc {
   int32_t cutoff;            /* m = AccuracyProfile.cutoff (1..8) */
   int32_t grid;              /* n = max(2m, even(ceil(oversampling*M))), nfft.py:151-153 */
   int32_t max_rhs;           /* largest nrhs passed to afs_apply (>= 1) */
-  /* 0: window values from degree-13 polynomials (|err| <= 2e-16 of the peak
-   *    value, below the reference's own sinh-argument rounding) feeding the
-   *    bin-sorted sliding-window kernels (default, fast);
+  /* 0: window values from per-offset polynomials (degree 11 at m >= 4, |err| <= 5e-16
+   *    of the peak value, below the reference's own 3.5e-15 sinh-argument rounding)
+   *    feeding the bin-sorted sliding-window kernels (default, fast);
    * 1: the reference's exact formula sinh(b s)/(pi s) evaluated per node with
    *    numpy's rounding order (slow parity mirror). */
   int32_t window_eval;

@@ -10,7 +10,7 @@
 // RED.E.ADD.F64 into the L2-resident grid) and entering cells loaded
 // (gather; the cell one step ahead is prefetched so the common one-cell
 // advance never waits on L2).  Per node, one lane evaluates the 2m*d window
-// values once (degree-13 polynomial, geometry.cuh) and stages them in shared
+// values once (per-table degree, kb_tables.inc / geometry.cuh) and stages them in shared
 // memory; the last dimension's values are stored pre-rotated into slot order
 // so the per-node work is a fixed, fully unrolled FMA sequence.
 //
