@@ -256,10 +256,14 @@ def run_ours(args):
     owner = lpt_assign(w.windows, w.N, w.m, world)
     mine = [i for i in range(w.P) if owner[i] == rank]
     my_windows = [w.windows[i] for i in mine]
+    torch.cuda.synchronize()
+    t_build0 = time.perf_counter()
     op = afs.AnovaKernelOperator(w.X, my_windows, w.sigma, afs.AccuracyProfile("c3", 2.0, w.m),
                                  None, afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
                                  weights=[1.0 / w.P] * len(mine), deterministic=args.deterministic)
     plan = op._plan
+    torch.cuda.synchronize()
+    plan_build_s = time.perf_counter() - t_build0
     alpha_host = w.alpha
     alpha = torch.from_numpy(alpha_host).to(dev)[None, :].contiguous()
     out = torch.empty((1, w.N), dtype=torch.float64, device=dev)
@@ -392,6 +396,7 @@ def run_ours(args):
                                     "frac_of_measured": Btot / (ms_step * 1e-3) / 1e9 / peak,
                                     "frac_of_8tbs": Btot / (ms_step * 1e-3) / 8e12},
             "stage_ms": stage,
+            "plan_build_s": plan_build_s,
             "roofline": {"bound": "hbm", "kernel": f"{kind} ({d}-D windows)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

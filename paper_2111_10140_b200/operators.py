@@ -135,6 +135,15 @@ def _columns_minmax(A, cols):
     return sub.amin(dim=0).cpu().numpy(), sub.amax(dim=0).cpu().numpy()
 
 
+def _all_columns_minmax(A):
+    """Per-column (mins, maxs) of the whole matrix in one pass; a window's bbox is the
+    subset of its columns (min/max are exact, so this equals fastsum.py:210-212 on X[:, w])."""
+    if isinstance(A, np.ndarray):
+        return A.min(axis=0), A.max(axis=0)
+    lo, hi = A.aminmax(dim=0)
+    return lo.cpu().numpy(), hi.cpu().numpy()
+
+
 def _as_matrix(A, name):
     if isinstance(A, np.ndarray) or not hasattr(A, "is_cuda"):
         A = np.asarray(A, dtype=np.float64)
@@ -178,15 +187,19 @@ class _Plan:
         descs = (_native.WindowDesc * len(feats))()
         self.n_windows = len(feats)
         self._keep = []
+        if scaling is None:
+            xlo, xhi = _all_columns_minmax(X)
+            if Z is not None:
+                zlo, zhi = _all_columns_minmax(Z)
         for l, (w, eta) in enumerate(zip(feats, weights)):
             if scaling is not None:
                 # externally fixed (e.g. bbox all-reduced over point shards)
                 center, scale = np.asarray(scaling[l][0], dtype=np.float64), float(scaling[l][1])
             else:
-                lo, hi = _columns_minmax(X, w)
+                cols = list(w)
+                lo, hi = xlo[cols], xhi[cols]
                 if Z is not None:
-                    zlo, zhi = _columns_minmax(Z, w)
-                    lo, hi = np.minimum(lo, zlo), np.maximum(hi, zhi)
+                    lo, hi = np.minimum(lo, zlo[cols]), np.maximum(hi, zhi[cols])
                 center, scale = bbox_scaling(lo, hi, config)
             if multipliers is not None:
                 # caller-supplied spectral multiplier (e.g. the bare NFFT: deconvolution only)
