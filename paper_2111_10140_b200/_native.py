@@ -14,6 +14,9 @@ import threading
 from .errors import DeviceError, NumericalError, ShapeError, ValidationError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libanovafs.so")
+# tuning hook: AFS_LIB selects an in-tree variant build (tools/build_variant.sh)
+if os.environ.get("AFS_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["AFS_LIB"])
 
 AFS_OK, AFS_ERR_SHAPE, AFS_ERR_VALIDATION, AFS_ERR_NUMERICAL, AFS_ERR_CUDA, AFS_ERR_NOMEM = range(6)
 

@@ -309,11 +309,13 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       p->src_side.assign(p->P, nullptr);
       p->tgt_side.assign(p->P, nullptr);
       for (int l = 0; l < p->P; ++l) {
+        const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab);
+        auto build = tc ? build_sorted_side_tc : build_sorted_side;
         p->src_side[l] = new SortedSide();
-        build_sorted_side(p, p->win[l], p->src, p->Ns, p->src_side[l]);
+        build(p, p->win[l], p->src, p->Ns, p->src_side[l]);
         if (p->has_targets) {
           p->tgt_side[l] = new SortedSide();
-          build_sorted_side(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l]);
+          build(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l]);
         }
       }
       int launches = 0;

@@ -148,6 +148,179 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
   cleanup();
 }
 
+// ---- tensor-core layout (2-D windows, tc2d.cuh) -------------------------------------------
+// Half-cell key: per dimension 2*u + c with u = floor(nx) mod n and c = (f > 1/2) the
+// reflection class the kernels apply (geometry.cuh poly_weights), last dimension fastest.
+__device__ __forceinline__ uint64_t half_cell_key(const double (&nx)[2], int n) {
+  uint64_t k = 0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const double fl = floor(nx[t]);
+    long long u = (long long)fl % n;
+    if (u < 0) u += n;
+    const int c = (nx[t] - fl) > 0.5 ? 1 : 0;
+    k = k * (uint64_t)(2 * n) + (uint64_t)(2 * u + c);
+  }
+  return k;
+}
+
+__global__ void k_prep_nodes_tc(const double* __restrict__ X, int64_t N, int dtot, Window w, int n,
+                                double* __restrict__ nx_out, uint64_t* __restrict__ key,
+                                int32_t* __restrict__ idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double nx[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const double xs = scaled_coord(X[j * dtot + w.feat[t]], w.center[t], w.scale);
+    nx[t] = __dmul_rn((double)n, xs);   // nfft.py:170
+    nx_out[t * N + j] = nx[t];
+  }
+  key[j] = half_cell_key(nx, n);
+  idx[j] = (int32_t)j;
+}
+
+__global__ void k_segment_counts(const uint64_t* __restrict__ key, int64_t N,
+                                 int32_t* __restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = i < N;
+  const unsigned long long k = live ? key[i] : ~0ULL;
+  const unsigned peers = __match_any_sync(0xffffffffu, k);
+  const int leader = __ffs(peers) - 1;
+  if (live && (int)(threadIdx.x & 31) == leader) atomicAdd(&counts[k], __popc(peers));
+}
+
+// sorted node i of segment s lands at pad_start[s] + (i - seg_start[s]); stores the
+// polynomial variable per dimension and, at group starts, the group header
+__global__ void k_scatter_tc(const double* __restrict__ nx_in, const int32_t* __restrict__ idx,
+                             const uint64_t* __restrict__ key, const int64_t* __restrict__ seg_start,
+                             const int64_t* __restrict__ pad_start, int64_t N, int64_t Npad, int n,
+                             double* __restrict__ x_out, int32_t* __restrict__ perm,
+                             int32_t* __restrict__ ghdr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const uint64_t s = key[i];
+  const int64_t dst = pad_start[s] + (i - seg_start[s]);
+  const int32_t j = idx[i];
+  perm[dst] = j;
+  int u[2], c[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const double nx = nx_in[t * N + j];
+    const double fl = floor(nx);
+    const double f = nx - fl;   // exact
+    c[t] = f > 0.5 ? 1 : 0;
+    long long uu = (long long)fl % n;
+    u[t] = (int)(uu < 0 ? uu + n : uu);
+    x_out[t * Npad + dst] = (c[t] ? __dsub_rn(1.0, f) : f) - 0.25;   // as poly_weights
+  }
+  if ((dst & 7) == 0) ghdr[dst >> 3] = tc_header(u[0], u[1], c[0], c[1]);
+}
+
+// padding slots: x = 0 (finite), perm -1 (no alpha, no output)
+__global__ void k_pad_tc(const int32_t* __restrict__ counts, const int64_t* __restrict__ pad_start,
+                         int64_t nseg, int64_t Npad, double* __restrict__ x, int32_t* __restrict__ perm) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int c = counts[s];
+  if (c == 0 || (c & 7) == 0) return;
+  const int64_t b = pad_start[s];
+  for (int k = c; k < ((c + 7) & ~7); ++k) {
+    perm[b + k] = -1;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) x[t * Npad + b + k] = 0.0;
+  }
+}
+
+bool tc_eligible(int d, int m, int tab) {
+  if (d != 2 || m != 4 || tab == 0) return false;
+  const char* e = getenv("AFS_TC");   // A/B hook: AFS_TC=0 keeps the FMA kernels
+  return !(e && e[0] == '0');
+}
+
+void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
+  if (N >= (int64_t)INT32_MAX / 2) throw Error(AFS_ERR_VALIDATION, "at most 2^30-1 nodes per plan");
+  if (w.d != 2) throw Error(AFS_ERR_VALIDATION, "tensor-core layout needs a 2-D window");
+  if (p->n > (1 << 14)) throw Error(AFS_ERR_VALIDATION, "tensor-core layout needs n <= 16384");
+  const int n = p->n;
+  const int64_t nseg = 4LL * n * n;
+  const cudaStream_t s = 0;
+  int bits = 1;
+  while ((1LL << bits) < nseg && bits < 63) ++bits;
+  double* nx_tmp = nullptr;
+  uint64_t *key_a = nullptr, *key_b = nullptr;
+  int32_t *idx_a = nullptr, *idx_b = nullptr, *counts = nullptr;
+  int64_t* starts = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  auto cleanup = [&] {
+    cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
+    cudaFree(counts); cudaFree(starts); cudaFree(temp);
+  };
+  try {
+    AFS_CUDA(cudaMalloc(&nx_tmp, sizeof(double) * 2 * std::max<int64_t>(N, 1)));
+    AFS_CUDA(cudaMalloc(&key_a, sizeof(uint64_t) * std::max<int64_t>(N, 1)));
+    AFS_CUDA(cudaMalloc(&key_b, sizeof(uint64_t) * std::max<int64_t>(N, 1)));
+    AFS_CUDA(cudaMalloc(&idx_a, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    AFS_CUDA(cudaMalloc(&idx_b, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * nseg));
+    AFS_CUDA(cudaMemset(counts, 0, sizeof(int32_t) * nseg));
+    const int th = 256;
+    const int64_t bl = (N + th - 1) / th;
+    if (N > 0) {
+      k_prep_nodes_tc<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, nx_tmp, key_a, idx_a);
+      AFS_CUDA(cudaGetLastError());
+      AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key_a, key_b, idx_a, idx_b,
+                                               (int)N, 0, bits, s));
+      AFS_CUDA(cudaMalloc(&temp, temp_bytes));
+      AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_a, key_b, idx_a, idx_b,
+                                               (int)N, 0, bits, s));
+      k_segment_counts<<<bl, th, 0, s>>>(key_b, N, counts);
+      AFS_CUDA(cudaGetLastError());
+    }
+    std::vector<int32_t> hc(nseg);
+    AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> hs(2 * nseg);   // [seg_start | pad_start]
+    int64_t pos = 0, pad = 0;
+    for (int64_t k = 0; k < nseg; ++k) {
+      hs[k] = pos;
+      hs[nseg + k] = pad;
+      pos += hc[k];
+      pad += (hc[k] + 7) & ~7;
+    }
+    const int64_t ngroups = pad / 8;
+    const int64_t Npad = pad + 8 * kTcTailGroups;   // trailing empty groups (tc2d.cuh)
+    AFS_CUDA(cudaMalloc(&starts, sizeof(int64_t) * 2 * nseg));
+    AFS_CUDA(cudaMemcpy(starts, hs.data(), sizeof(int64_t) * 2 * nseg, cudaMemcpyHostToDevice));
+    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 2 * std::max<int64_t>(Npad, 1)));
+    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * std::max<int64_t>(Npad, 1)));
+    AFS_CUDA(cudaMalloc(&out->ghdr, sizeof(int32_t) * (Npad / 8)));
+    AFS_CUDA(cudaMemset(out->ghdr, 0, sizeof(int32_t) * (Npad / 8)));
+    AFS_CUDA(cudaMemset(out->nx, 0, sizeof(double) * 2 * Npad));
+    AFS_CUDA(cudaMemset(out->perm, 0xff, sizeof(int32_t) * Npad));   // -1: no node
+    if (N > 0) {
+      k_scatter_tc<<<bl, th, 0, s>>>(nx_tmp, idx_b, key_b, starts, starts + nseg, N, Npad, n, out->nx,
+                                     out->perm, out->ghdr);
+      AFS_CUDA(cudaGetLastError());
+      k_pad_tc<<<(unsigned)((nseg + th - 1) / th), th, 0, s>>>(counts, starts + nseg, nseg, Npad,
+                                                               out->nx, out->perm);
+      AFS_CUDA(cudaGetLastError());
+    }
+    out->N = Npad;
+    out->n_real = N;
+    out->ngroups = ngroups;
+    out->tc = true;
+    out->nchunks = 0;
+    out->chunk_cap = 0;
+    p->device_bytes += (int64_t)(sizeof(double) * 2 + sizeof(int32_t)) * Npad + (int64_t)sizeof(int32_t) * (Npad / 8);
+    AFS_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
 int kb_table_id(int M, int n) {
   if (n == 2 * M) return 1;
   if (2 * n == 3 * M) return 2;
@@ -155,6 +328,7 @@ int kb_table_id(int M, int n) {
 }
 
 void free_sorted_side(SortedSide* s) {
+  cudaFree(s->ghdr);
   cudaFree(s->nx);
   cudaFree(s->perm);
   cudaFree(s->chunks);

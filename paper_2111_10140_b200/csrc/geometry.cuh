@@ -33,14 +33,34 @@ struct Chunk {
 struct SortedSide {
   int64_t N = 0;
   double* nx = nullptr;      // [d][N]: n * scaled coordinate, sorted by cell
-  int32_t* perm = nullptr;   // [N]: sorted position -> original node index
+  int32_t* perm = nullptr;   // [N]: sorted position -> original node index (-1: padding)
   Chunk* chunks = nullptr;   // device
   int64_t nchunks = 0;
   int chunk_cap = 0;
+  // tensor-core layout (tc2d.cuh): sorted by half-cell (base cell + reflection class per
+  // dimension), every half-cell padded to a multiple of 8 nodes, so that each group of 8
+  // consecutive nodes shares one stencil.  nx then holds the polynomial variable
+  // x = (c ? 1 - f : f) - 1/4 of poly_weights instead of n*x, and ghdr[N/8] the group's
+  // stencil (tc_header); N counts the padding, n_real does not
+  bool tc = false;
+  int64_t n_real = 0;
+  int32_t* ghdr = nullptr;
+  int64_t ngroups = 0;   // groups of 8 holding nodes; N / 8 - ngroups >= kTcTailGroups empty ones follow
+  __host__ __device__ const double* x0() const { return nx; }
+  __host__ __device__ const double* x1() const { return nx + N; }
 };
 
 void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
                        SortedSide* out);
+void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N,
+                          SortedSide* out);
+bool tc_eligible(int d, int m, int tab);
+constexpr int kTcTailGroups = 16;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
+
+// group header of the tensor-core layout: wrapped base cells and reflection classes
+__host__ __device__ __forceinline__ int32_t tc_header(int u0, int u1, int c0, int c1) {
+  return u0 | (u1 << 14) | (c0 << 28) | (c1 << 29);
+}
 void free_sorted_side(SortedSide* s);
 void make_poly_table(int m, double b, PolyTable* t);
 int kb_table_id(int M, int n);   // 1: n = 2M, 2: 2n = 3M, 0: run-time table

@@ -8,6 +8,7 @@
 
 #include "afs_internal.cuh"
 #include "sliding.cuh"
+#include "tc2d.cuh"
 
 namespace afs {
 
@@ -84,6 +85,7 @@ static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t ld
   if (p->window_eval != 0) return false;
   const Window& w = p->win[l];
   const SortedSide& sv = *p->src_side[l];
+  if (sv.tc) return launch_spread_tc(sv, w, p->n, p->kb_tab, alpha, lda, R, p->grids, p->grid_total, s);
   const int rg = v2_rhs_group(w.d, p->m, R);
   if (rg < 1) return false;
   for (int r0 = 0; r0 < R; r0 += rg) {

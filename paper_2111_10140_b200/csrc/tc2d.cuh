@@ -1,0 +1,398 @@
+// Spread / gather for 2-D windows at m = 4 on the fp64 tensor cores (DMMA, mma.sync
+// m8n8k4 f64).
+//
+// Nodes are sorted by half-cell -- base cell u = floor(n x) and reflection class
+// c = (f > 1/2) per dimension -- and every half-cell is padded to a multiple of 8 nodes
+// (build_sorted_side_tc), so each group of 8 consecutive nodes shares one 8x8 stencil.
+// Per group and dimension the window values are one matrix product
+//     Phi[node][o] = sum_k x_node^k C[o][k]      (8 nodes x 12 terms x 8 offsets)
+// with x = (c ? 1 - f : f) - 1/4 (stored at plan time) and C the constant-bank KB polynomial table
+// (geometry.cuh poly_weights), i.e. three DMMAs.  The reflection only permutes the
+// stencil (phi(f + m-1-o) = P_{7-o}(x) when c = 1), which the kernels fold into the grid
+// addressing.  The tensor-product touch is two more DMMAs:
+//     gather  s_node  = sum_p (Phi_x G)[node][p] Phi_y[node][p]        (nfft.py:228-229)
+//     spread  G[o][p] += sum_node alpha_node Phi_x[node][o] Phi_y[node][p] (nfft.py:241-245)
+// The fragment layouts line up without shuffles: the eval result D[row][2q+t] is directly
+// the A (gather) or, evaluated transposed, the A/B (spread) operand of the touch MMA with
+// k relabelled as offset (or node) 2k+t.  Per group: 8 DMMAs = 2048 fp64 MACs, against
+// ~1980 DFMAs of the lane-private FMA kernels (solo.cuh) -- the same arithmetic, but one
+// instruction per 256 MACs, so the fp64 pipe stops waiting on issue.
+#pragma once
+
+#include <algorithm>
+
+#ifndef AFS_TC_MINB
+#define AFS_TC_MINB 1   // __launch_bounds__ min blocks per SM (register cap), tuning hook
+#endif
+
+#include "geometry.cuh"
+#include "sliding.cuh"
+
+namespace afs {
+
+// d[0..1] += A(8x4) B(4x8): lane holds a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// d = D[lane/4][2(lane%4) + {0,1}].  Not volatile: independent groups may interleave.
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+template <int TAB>
+struct TcPoly {
+  static constexpr int NT = kb_terms<TAB, 4>();
+  static constexpr int NKS = (NT + 3) / 4;   // k-steps of 4 terms
+};
+
+// lane's coefficient fragment: C[o = lane/4][k = lane%4 + 4s].  Laundered through a
+// volatile move so ptxas keeps it in registers instead of re-reading the constant bank
+// (divergent LDC) every iteration.
+template <int TAB>
+__device__ __forceinline__ void tc_coefs(int lane, double (&cf)[TcPoly<TAB>::NKS]) {
+  constexpr int NT = TcPoly<TAB>::NT;
+#pragma unroll
+  for (int s = 0; s < TcPoly<TAB>::NKS; ++s) {
+    const int k = (lane & 3) + 4 * s;
+    const double c = k < NT ? kb_coef<TAB, 4>(lane >> 2, k) : 0.0;
+    asm volatile("mov.b64 %0, %1;" : "=d"(cf[s]) : "d"(c));
+  }
+}
+
+// lane's power fragment x^(q + 4s), q = lane % 4 (q1: q odd, q2: q >= 2)
+template <int NKS>
+__device__ __forceinline__ void tc_powers(double x, bool q1, bool q2, double (&pw)[NKS]) {
+  const double x2 = x * x;
+  const double x4 = x2 * x2;
+  const double p0 = (q1 ? x : 1.0) * (q2 ? x2 : 1.0);
+  pw[0] = p0;
+  if constexpr (NKS > 1) pw[1] = p0 * x4;
+  if constexpr (NKS > 2) pw[2] = pw[1] * x4;
+  if constexpr (NKS > 3) pw[3] = pw[2] * x4;
+}
+
+// grid cell of stencil slot o (polynomial order) for wrapped base cell u, class c (m = 4):
+// u - 3 + (c ? 7 - o : o) mod n; 7 - o = o ^ 7.  POW2: n is a power of two (mask n - 1)
+template <bool POW2>
+__device__ __forceinline__ int tc_cell(int u, int c, int o, int n) {
+  const int v = u - 3 + (o ^ (c ? 7 : 0));
+  if constexpr (POW2) return v & (n - 1);
+  else return wrap_cell(v, n);
+}
+__device__ __forceinline__ int tc_u0(int32_t h) { return h & 0x3fff; }
+__device__ __forceinline__ int tc_u1(int32_t h) { return (h >> 14) & 0x3fff; }
+__device__ __forceinline__ int tc_c0(int32_t h) { return (h >> 28) & 1; }
+__device__ __forceinline__ int tc_c1(int32_t h) { return (h >> 29) & 1; }
+
+// ---------------------------------------------------------------------------
+// Node stream.  A warp walks its groups U at a time ("batches") through a per-warp
+// shared-memory ring of D batches filled with cp.async, so no registers are held for
+// loads in flight:
+//   iteration b stages the node data (x0, x1, perm, header) of batch b + D, and the
+//   random per-node values of batch b + 2 (out[perm] in the gather, alpha[perm] in the
+//   spread; their perm landed two iterations earlier);
+//   the grid window operands of batch b + 1 (gather) are loaded into registers.
+// ---------------------------------------------------------------------------
+template <int U, int D, int RG>
+struct TcRing {
+  double x0[D][8 * U];
+  double x1[D][8 * U];
+  double val[D][RG][8 * U];
+  int32_t perm[D][8 * U];
+  alignas(16) int32_t hdr[D][U];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// node data of batch gb (groups gb .. gb+U-1) into slot st, 16 B chunks: [0,4U) x0,
+// [4U,8U) x1, [8U,10U) perm, then the U headers (4U bytes; gb is a multiple of U)
+template <int U, int D, int RG>
+__device__ __forceinline__ void tc_stage_nodes(TcRing<U, D, RG>& R, int st, const SortedSide& sv,
+                                               int gb, int lane) {
+  static_assert(U == 1 || U == 2 || U == 4, "batch of 1, 2 or 4 groups");
+  const int i0 = gb * 8;
+#pragma unroll
+  for (int c = lane; c < 10 * U + 1; c += 32) {
+    if (c < 4 * U) {
+      cp_async16(&R.x0[st][2 * c], sv.x0() + i0 + 2 * c);
+    } else if (c < 8 * U) {
+      cp_async16(&R.x1[st][2 * (c - 4 * U)], sv.x1() + i0 + 2 * (c - 4 * U));
+    } else if (c < 10 * U) {
+      cp_async16(&R.perm[st][4 * (c - 8 * U)], sv.perm + i0 + 4 * (c - 8 * U));
+    } else {
+      if constexpr (U == 4) cp_async16(&R.hdr[st][0], sv.ghdr + gb);
+      else if constexpr (U == 2) cp_async8(&R.hdr[st][0], sv.ghdr + gb);
+      else cp_async4(&R.hdr[st][0], sv.ghdr + gb);
+    }
+  }
+}
+
+// per-node values src[r * ld + perm] of the batch in slot st (its perm has landed);
+// padding nodes get 0.  Lane l copies node l of the batch (8U <= 32 nodes).
+template <int U, int D, int RG>
+__device__ __forceinline__ void tc_stage_vals(TcRing<U, D, RG>& R, int st, const double* src,
+                                              int64_t ld, int nr, int lane) {
+  if (lane < 8 * U) {
+    const int j = R.perm[st][lane];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      if (j >= 0 && r < nr) cp_async8(&R.val[st][r][lane], src + r * ld + j);
+      else R.val[st][r][lane] = 0.0;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// gather: out[perm] += eta * interp over groups [g0, g1) of one warp, U at a time
+// ----------------------------------------------------------------------------
+template <int RG, int TAB, int U, bool POW2, int D>
+__global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide sv, const Window w, int n,
+                                                   const double* __restrict__ grid,
+                                                   int64_t rhs_stride, int nr,
+                                                   double* __restrict__ out, int64_t ldo,
+                                                   int gpw) {
+  static_assert(D >= 4, "values are staged two batches ahead of node data landing");
+  constexpr int NKS = TcPoly<TAB>::NKS;
+  __shared__ TcRing<U, D, RG> ring[4];
+  const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
+  const bool q1 = q & 1, q2 = q >= 2;
+  TcRing<U, D, RG>& R = ring[threadIdx.x >> 5];
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g0 = warp * gpw;
+  if (g0 >= sv.ngroups) return;   // warp-uniform
+  // gpw is a multiple of U and the layout carries >= D*U trailing empty groups, so the last
+  // warp may run (and prefetch) past ngroups without clamping
+  const int g1 = min(g0 + gpw, (int)sv.ngroups);
+  double cf[NKS];
+  tc_coefs<TAB>(lane, cf);
+  const double* g = grid + w.grid_off;
+
+  // grid operands of one batch: B[k][p] = G[cell(o = 2k + t)][cell(p)], k = lane%4, p = lane/4
+  struct Win {
+    double ga[U][RG], gc[U][RG];
+  };
+  auto load_win = [&](int st, Win& d) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t h = R.hdr[st][u];
+      const int col = tc_cell<POW2>(tc_u1(h), tc_c1(h), slot, n);
+      const int ra = tc_cell<POW2>(tc_u0(h), tc_c0(h), 2 * q, n) * n + col;
+      const int rb = tc_cell<POW2>(tc_u0(h), tc_c0(h), 2 * q + 1, n) * n + col;
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        const double* gr = g + (r < nr ? r : 0) * rhs_stride;
+        d.ga[u][r] = __ldg(gr + ra);
+        d.gc[u][r] = __ldg(gr + rb);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    tc_stage_nodes(R, k, sv, g0 + k * U, lane);
+    cp_async_commit();
+  }
+  cp_async_wait<D - 2>();
+  __syncwarp();
+  tc_stage_vals(R, 0, out, ldo, nr, lane);
+  tc_stage_vals(R, 1, out, ldo, nr, lane);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  Win wnext;
+  load_win(0, wnext);
+  int st = 0;
+#pragma unroll 1
+  for (int gb = g0; gb < g1; gb += U) {
+    cp_async_wait<1>();   // node data up to batch b + 2 and values of batch b have landed
+    __syncwarp();
+    double x0[U], x1[U], prior[U][RG];
+    int j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x0[u] = R.x0[st][u * 8 + slot];
+      x1[u] = R.x1[st][u * 8 + slot];
+      j[u] = R.perm[st][u * 8 + slot];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) prior[u][r] = R.val[st][r][u * 8 + slot];
+    }
+    const Win wcur = wnext;
+    const int st1 = st + 1 == D ? 0 : st + 1;
+    const int st2 = st1 + 1 == D ? 0 : st1 + 1;
+    __syncwarp();
+    tc_stage_nodes(R, st, sv, gb + D * U, lane);   // refill the slot just read
+    tc_stage_vals(R, st2, out, ldo, nr, lane);       // values of batch b + 2
+    cp_async_commit();
+    load_win(st1, wnext);                            // grid window of batch b + 1
+    // window values Phi[node][o], o = 2q, 2q+1
+    double fx[U][2], fy[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double px[NKS], py[NKS];
+      tc_powers<NKS>(x0[u], q1, q2, px);
+      tc_powers<NKS>(x1[u], q1, q2, py);
+      fx[u][0] = fx[u][1] = fy[u][0] = fy[u][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < NKS; ++s) {
+        dmma884(fx[u], px[s], cf[s]);
+        dmma884(fy[u], py[s], cf[s]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        double t[2] = {0.0, 0.0};
+        dmma884(t, fx[u][0], wcur.ga[u][r]);
+        dmma884(t, fx[u][1], wcur.gc[u][r]);
+        double s = fma(t[1], fy[u][1], t[0] * fy[u][0]);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (q == 0 && j[u] >= 0 && r < nr)
+          out[r * ldo + j[u]] = __dadd_rn(prior[u][r], __dmul_rn(w.eta, s));
+      }
+    }
+    st = st1;
+  }
+  cp_async_wait<0>();
+}
+
+// ----------------------------------------------------------------------------
+// spread: grid += sum_node alpha_node Phi_x (x) Phi_y, accumulated per half-cell in the
+// MMA accumulators (one per group of the batch, summed at the flush) and flushed
+// (RED.F64 / fixed-point limbs) when the group header changes
+// ----------------------------------------------------------------------------
+template <int RG, int TAB, int U, bool POW2, int D>
+__global__ void __launch_bounds__(128, AFS_TC_MINB) k_spread_tc(const SortedSide sv, const Window w, int n,
+                                                   const double* __restrict__ alpha, int64_t lda,
+                                                   int nr, double* __restrict__ grid,
+                                                   int64_t rhs_stride, int gpw) {
+  static_assert(D >= 4, "values are staged two batches ahead of node data landing");
+  constexpr int NKS = TcPoly<TAB>::NKS;
+  __shared__ TcRing<U, D, RG> ring[4];
+  const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
+  const bool q1 = q & 1, q2 = q >= 2;
+  TcRing<U, D, RG>& R = ring[threadIdx.x >> 5];
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g0 = warp * gpw;
+  if (g0 >= sv.ngroups) return;   // warp-uniform
+  const int g1 = min(g0 + gpw, (int)sv.ngroups);
+  double cf[NKS];
+  tc_coefs<TAB>(lane, cf);
+  double* g = grid + w.grid_off;
+
+  double acc[U][RG][2];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int r = 0; r < RG; ++r) acc[u][r][0] = acc[u][r][1] = 0.0;
+  int32_t cur_h = -1;
+  // lane holds acc[o = slot][p = 2q + e]
+  auto flush = [&]() {
+    const int row = tc_cell<POW2>(tc_u0(cur_h), tc_c0(cur_h), slot, n) * n;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ix = row + tc_cell<POW2>(tc_u1(cur_h), tc_c1(cur_h), 2 * q + e, n);
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        double v = acc[0][r][e];
+        acc[0][r][e] = 0.0;
+#pragma unroll
+        for (int u = 1; u < U; ++u) {
+          v += acc[u][r][e];
+          acc[u][r][e] = 0.0;
+        }
+        if (r < nr && v != 0.0) grid_add(w, g + r * rhs_stride + ix, v);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    tc_stage_nodes(R, k, sv, g0 + k * U, lane);
+    cp_async_commit();
+  }
+  cp_async_wait<D - 2>();
+  __syncwarp();
+  tc_stage_vals(R, 0, alpha, lda, nr, lane);
+  tc_stage_vals(R, 1, alpha, lda, nr, lane);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  int st = 0;
+#pragma unroll 1
+  for (int gb = g0; gb < g1; gb += U) {
+    cp_async_wait<1>();
+    __syncwarp();
+    double x0[U], x1[U], al[U][RG][2];
+    int32_t hd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x0[u] = R.x0[st][u * 8 + slot];
+      x1[u] = R.x1[st][u * 8 + slot];
+      hd[u] = R.hdr[st][u];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {   // alpha of the lane's k-nodes 2q, 2q+1
+        const double2 a2 = *reinterpret_cast<const double2*>(&R.val[st][r][u * 8 + 2 * q]);
+        al[u][r][0] = a2.x;
+        al[u][r][1] = a2.y;
+      }
+    }
+    const int st1 = st + 1 == D ? 0 : st + 1;
+    const int st2 = st1 + 1 == D ? 0 : st1 + 1;
+    __syncwarp();
+    tc_stage_nodes(R, st, sv, gb + D * U, lane);
+    tc_stage_vals(R, st2, alpha, lda, nr, lane);
+    cp_async_commit();
+    // transposed window values: Phi[node][o] held as D[o = slot][node = 2q + t]
+    double fx[U][2], fy[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double px[NKS], py[NKS];
+      tc_powers<NKS>(x0[u], q1, q2, px);
+      tc_powers<NKS>(x1[u], q1, q2, py);
+      fx[u][0] = fx[u][1] = fy[u][0] = fy[u][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < NKS; ++s) {
+        dmma884(fx[u], cf[s], px[s]);
+        dmma884(fy[u], cf[s], py[s]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (hd[u] != cur_h) {   // warp-uniform
+        if (cur_h != -1) flush();
+        cur_h = hd[u];
+      }
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        dmma884(acc[u][r], fx[u][0] * al[u][r][0], fy[u][0]);
+        dmma884(acc[u][r], fx[u][1] * al[u][r][1], fy[u][1]);
+      }
+    }
+    st = st1;
+  }
+  cp_async_wait<0>();
+  if (cur_h != -1) flush();
+}
+
+// host launchers (tc2d.cu); false when the window is not in the tensor-core layout
+bool launch_spread_tc(const SortedSide& sv, const Window& w, int n, int tab, const double* alpha,
+                      int64_t lda, int R, double* grid, int64_t rs, cudaStream_t s);
+bool launch_gather_tc(const SortedSide& sv, const Window& w, int n, int tab, const double* grid,
+                      int64_t rs, int R, double* out, int64_t ldo, cudaStream_t s);
+
+}  // namespace afs
