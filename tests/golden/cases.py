@@ -12,6 +12,11 @@ FASTSUM_CASES = [
     ("fs_d3_M16_m3_os15", 3, 16, 3, 1.5, 0.2, 300, 0),
     ("fs_d3_M32_m4", 3, 32, 4, 2.0, 1.0, 800, 0),
     ("fs_d3_M16_m4_tgt", 3, 16, 4, 2.0, 0.4, 500, 350),
+    # 2-D windows at m = 4 take the fp64 tensor-core kernels (csrc/tc2d.cuh): targets,
+    # a non-power-of-two grid (n = 48, second compile-time table), many nodes per half-cell
+    ("fs_d2_M32_m4_tgt", 2, 32, 4, 2.0, 0.3, 2000, 700),
+    ("fs_d2_M32_m4_os15", 2, 32, 4, 1.5, 0.3, 1500, 0),
+    ("fs_d2_M16_m4_dense", 2, 16, 4, 2.0, 0.2, 20000, 0),
 ]
 
 
