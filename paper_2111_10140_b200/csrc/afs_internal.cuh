@@ -113,6 +113,13 @@ struct afs_plan {
   std::vector<afs::GraphEntry> graphs;
   cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // second branch of the spread / gather stages: windows alternate between the stage's
+  // stream and this one, so one window's tail overlaps the next window's kernel (spread
+  // grids are disjoint; the gather's odd windows accumulate into out2, added at the join)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int stage_streams = 2;
+  double* out2 = nullptr;           // [max_rhs][Nt]
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};
@@ -134,6 +141,7 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
 void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
                    int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
 void make_twiddles(afs_plan* p);
+void ensure_aux_stream(afs_plan* p);
 
 // ---------------------------------------------------------------------------
 // grid accumulation of the spread

@@ -134,6 +134,16 @@ static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R
   return true;
 }
 
+__global__ void k_add_into(double* __restrict__ out, int64_t ldo, const double* __restrict__ add,
+                           int64_t lda, int64_t N, int R) {
+  const int64_t tot = N * R;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < tot;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / N, i = k - r * N;
+    out[r * ldo + i] += add[r * lda + i];
+  }
+}
+
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
   // out = 0, then out += eta_l * s_l in window order (anova.py:179-183)
   AFS_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * p->Nt, R, s));
@@ -141,11 +151,39 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
     gather_v1(p, 0, p->P, out, ldo, R, s);
   } else {
     const bool timed = p->profiling && !p->wev_gather.empty();
+    // two branches (as the spread, spread.cu): odd windows accumulate into the plan's second
+    // output buffer on the aux stream, added at the join -- out = sum over even windows +
+    // sum over odd windows, each in window order (fixed, so run-to-run reproducible).  Only
+    // while both accumulators stay L2-resident: their random read-modify-writes otherwise
+    // compete for L2 and the overlap is lost (C3: 2 x 80 MB, measured slower)
+    const bool fork = !timed && p->stage_streams > 1 && p->P > 1 &&
+                      2 * p->Nt * R * (int64_t)sizeof(double) <= (64LL << 20);
+    if (fork) {
+      ensure_aux_stream(p);
+      if (!p->out2) {
+        AFS_CUDA(cudaMalloc(&p->out2, sizeof(double) * p->Nt * p->max_rhs));
+        p->device_bytes += sizeof(double) * p->Nt * p->max_rhs;
+      }
+      AFS_CUDA(cudaEventRecord(p->ev_fork, s));
+      AFS_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+      AFS_CUDA(cudaMemsetAsync(p->out2, 0, sizeof(double) * p->Nt * R, p->aux));
+    }
     for (int l = 0; l < p->P; ++l) {
       if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
-      if (!gather_v2_window(p, l, out, ldo, R, s)) gather_v1(p, l, l + 1, out, ldo, R, s);
+      const bool odd = fork && (l & 1);
+      const cudaStream_t sl = odd ? p->aux : s;
+      double* o = odd ? p->out2 : out;
+      const int64_t lo = odd ? p->Nt : ldo;
+      if (!gather_v2_window(p, l, o, lo, R, sl)) gather_v1(p, l, l + 1, o, lo, R, sl);
     }
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
+    if (fork) {
+      AFS_CUDA(cudaEventRecord(p->ev_join, p->aux));
+      AFS_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+      const int64_t tot = p->Nt * R;
+      const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+      k_add_into<<<blocks, 256, 0, s>>>(out, ldo, p->out2, p->Nt, p->Nt, R);
+    }
   }
   AFS_CUDA(cudaGetLastError());
 }

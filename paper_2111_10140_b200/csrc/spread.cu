@@ -164,6 +164,13 @@ __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stri
   grids[i] = (neg ? -mag : mag) * aux[2];
 }
 
+void ensure_aux_stream(afs_plan* p) {
+  if (p->aux) return;
+  AFS_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+  AFS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  AFS_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+}
+
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
   const bool det = p->deterministic && p->det_limbs;
   const int64_t cells = p->grid_total * R;
@@ -179,20 +186,32 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
     AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * cells, s));
   }
   const bool timed = p->profiling && !p->wev_spread.empty();
+  // two branches (not while timing windows): window l runs on branch l % 2
+  const bool fork = !timed && p->stage_streams > 1 && p->P > 1 && p->window_eval == 0;
+  if (fork) {
+    ensure_aux_stream(p);
+    AFS_CUDA(cudaEventRecord(p->ev_fork, s));
+    AFS_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+  }
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[l], s));
-    if (spread_v2_window(p, l, alpha, lda, R, s)) continue;
+    const cudaStream_t sl = (fork && (l & 1)) ? p->aux : s;
+    if (spread_v2_window(p, l, alpha, lda, R, sl)) continue;
     switch (p->m) {
-      case 1: launch_spread_m<1>(p, w, alpha, lda, R, s); break;
-      case 2: launch_spread_m<2>(p, w, alpha, lda, R, s); break;
-      case 3: launch_spread_m<3>(p, w, alpha, lda, R, s); break;
-      case 4: launch_spread_m<4>(p, w, alpha, lda, R, s); break;
-      case 5: launch_spread_m<5>(p, w, alpha, lda, R, s); break;
-      case 6: launch_spread_m<6>(p, w, alpha, lda, R, s); break;
-      case 7: launch_spread_m<7>(p, w, alpha, lda, R, s); break;
-      default: launch_spread_m<8>(p, w, alpha, lda, R, s); break;
+      case 1: launch_spread_m<1>(p, w, alpha, lda, R, sl); break;
+      case 2: launch_spread_m<2>(p, w, alpha, lda, R, sl); break;
+      case 3: launch_spread_m<3>(p, w, alpha, lda, R, sl); break;
+      case 4: launch_spread_m<4>(p, w, alpha, lda, R, sl); break;
+      case 5: launch_spread_m<5>(p, w, alpha, lda, R, sl); break;
+      case 6: launch_spread_m<6>(p, w, alpha, lda, R, sl); break;
+      case 7: launch_spread_m<7>(p, w, alpha, lda, R, sl); break;
+      default: launch_spread_m<8>(p, w, alpha, lda, R, sl); break;
     }
+  }
+  if (fork) {
+    AFS_CUDA(cudaEventRecord(p->ev_join, p->aux));
+    AFS_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
   }
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   if (det) {
