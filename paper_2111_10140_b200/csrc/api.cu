@@ -313,16 +313,24 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       p->kb_tab = kb_table_id(p->M, p->n);
       p->src_side.assign(p->P, nullptr);
       p->tgt_side.assign(p->P, nullptr);
-      for (int l = 0; l < p->P; ++l) {
-        const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab);
-        auto build = tc ? build_sorted_side_tc : build_sorted_side;
-        p->src_side[l] = new SortedSide();
-        build(p, p->win[l], p->src, p->Ns, p->src_side[l]);
-        if (p->has_targets) {
-          p->tgt_side[l] = new SortedSide();
-          build(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l]);
+      BuildScratch sc;   // sort temporaries shared by all windows
+      try {
+        for (int l = 0; l < p->P; ++l) {
+          const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab);
+          auto build = tc ? build_sorted_side_tc : build_sorted_side;
+          p->src_side[l] = new SortedSide();
+          build(p, p->win[l], p->src, p->Ns, p->src_side[l], sc);
+          if (p->has_targets) {
+            p->tgt_side[l] = new SortedSide();
+            build(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l], sc);
+          }
         }
+        AFS_CUDA(cudaDeviceSynchronize());
+      } catch (...) {
+        sc.release();
+        throw;
       }
+      sc.release();
       int launches = 0;
       for (const Window& w : p->win) launches += 2 + (w.d == 1 ? 1 : (w.d == 2 ? 3 : 5));
       p->launches_per_apply = launches;

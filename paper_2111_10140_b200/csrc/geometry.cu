@@ -74,7 +74,47 @@ static int chunk_cap_for(int d, int64_t N) {
   return (int)std::max<int64_t>(64, std::min<int64_t>(hi, cap));
 }
 
-void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
+void BuildScratch::reserve(int64_t N, int d) {
+  N = std::max<int64_t>(N, 1);
+  if (N <= cap && d <= 3) return;
+  cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
+  nx_tmp = nullptr; key_a = key_b = nullptr; idx_a = idx_b = nullptr; cap = 0;
+  AFS_CUDA(cudaMalloc(&nx_tmp, sizeof(double) * 3 * N));
+  AFS_CUDA(cudaMalloc(&key_a, sizeof(uint64_t) * N));
+  AFS_CUDA(cudaMalloc(&key_b, sizeof(uint64_t) * N));
+  AFS_CUDA(cudaMalloc(&idx_a, sizeof(int32_t) * N));
+  AFS_CUDA(cudaMalloc(&idx_b, sizeof(int32_t) * N));
+  cap = N;
+}
+
+void BuildScratch::reserve_counts(int64_t n) {
+  if (n <= counts_cap) return;
+  cudaFree(counts); cudaFree(starts);
+  counts = nullptr; starts = nullptr; counts_cap = 0;
+  AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * n));
+  AFS_CUDA(cudaMalloc(&starts, sizeof(int64_t) * 2 * n));
+  counts_cap = n;
+}
+
+void* BuildScratch::sort_temp(size_t bytes) {
+  if (bytes > temp_bytes) {
+    cudaFree(temp);
+    temp = nullptr;
+    temp_bytes = 0;
+    AFS_CUDA(cudaMalloc(&temp, bytes));
+    temp_bytes = bytes;
+  }
+  return temp;
+}
+
+void BuildScratch::release() {
+  cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
+  cudaFree(temp); cudaFree(counts); cudaFree(starts);
+  *this = BuildScratch{};
+}
+
+void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                       BuildScratch& sc) {
   if (N >= (int64_t)INT32_MAX) throw Error(AFS_ERR_VALIDATION, "at most 2^31-1 nodes per plan");
   const int d = w.d, n = p->n;
   const cudaStream_t s = 0;
@@ -84,68 +124,50 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
     for (int t = 0; t < d; ++t) cells *= n;
     while ((long double)(1ULL << bits) < cells && bits < 63) ++bits;
   }
-  double* nx_tmp = nullptr;
-  uint64_t *key_a = nullptr, *key_b = nullptr;
-  int32_t *idx_a = nullptr, *idx_b = nullptr, *counts = nullptr;
-  void* temp = nullptr;
+  sc.reserve(N, d);
+  const int64_t ncol = d == 1 ? 1 : (d == 2 ? (int64_t)n : (int64_t)n * n);
+  sc.reserve_counts(ncol);
+  const int th = 256;
+  const int64_t bl = (N + th - 1) / th;
+  k_prep_nodes<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, sc.nx_tmp, sc.key_a, sc.idx_a);
+  AFS_CUDA(cudaGetLastError());
   size_t temp_bytes = 0;
-  auto cleanup = [&] {
-    cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
-    cudaFree(counts); cudaFree(temp);
-  };
-  try {
-    AFS_CUDA(cudaMalloc(&nx_tmp, sizeof(double) * d * N));
-    AFS_CUDA(cudaMalloc(&key_a, sizeof(uint64_t) * N));
-    AFS_CUDA(cudaMalloc(&key_b, sizeof(uint64_t) * N));
-    AFS_CUDA(cudaMalloc(&idx_a, sizeof(int32_t) * N));
-    AFS_CUDA(cudaMalloc(&idx_b, sizeof(int32_t) * N));
-    const int th = 256;
-    const int64_t bl = (N + th - 1) / th;
-    k_prep_nodes<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, nx_tmp, key_a, idx_a);
-    AFS_CUDA(cudaGetLastError());
-    AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key_a, key_b, idx_a, idx_b,
-                                             (int)N, 0, bits > 0 ? bits : 1, s));
-    AFS_CUDA(cudaMalloc(&temp, temp_bytes));
-    AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_a, key_b, idx_a, idx_b,
-                                             (int)N, 0, bits > 0 ? bits : 1, s));
-    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * d * N));
-    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * N));
-    k_permute_nodes<<<bl, th, 0, s>>>(nx_tmp, idx_b, N, d, out->nx, out->perm);
-    AFS_CUDA(cudaGetLastError());
-    // column runs
-    const int64_t ncol = d == 1 ? 1 : (d == 2 ? (int64_t)n : (int64_t)n * n);
-    AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * ncol));
-    AFS_CUDA(cudaMemset(counts, 0, sizeof(int32_t) * ncol));
-    k_column_counts<<<bl, th, 0, s>>>(key_b, N, (uint64_t)n, counts);
-    AFS_CUDA(cudaGetLastError());
-    std::vector<int32_t> hc(ncol);
-    AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * ncol, cudaMemcpyDeviceToHost));
-    const int cap = chunk_cap_for(d, N);
-    std::vector<Chunk> ch;
-    int64_t pos = 0;
-    for (int64_t c = 0; c < ncol; ++c) {
-      for (int32_t o = 0; o < hc[c]; o += cap)
-        ch.push_back(Chunk{(int32_t)c, std::min(cap, hc[c] - o), pos + o, 0, 0});
-      pos += hc[c];
-    }
-    out->N = N;
-    out->nchunks = (int64_t)ch.size();
-    out->chunk_cap = cap;
-    AFS_CUDA(cudaMalloc(&out->chunks, sizeof(Chunk) * std::max<size_t>(1, ch.size())));
-    AFS_CUDA(cudaMemcpy(out->chunks, ch.data(), sizeof(Chunk) * ch.size(), cudaMemcpyHostToDevice));
-    if (!ch.empty()) {
-      k_chunk_cell0<<<(unsigned)((ch.size() + 255) / 256), 256, 0, s>>>(
-          out->chunks, (int64_t)ch.size(), out->nx + (int64_t)(d - 1) * N, n);
-      AFS_CUDA(cudaGetLastError());
-    }
-    p->device_bytes += (int64_t)(sizeof(double) * d + sizeof(int32_t)) * N +
-                       (int64_t)sizeof(Chunk) * out->nchunks;
-    AFS_CUDA(cudaDeviceSynchronize());
-  } catch (...) {
-    cleanup();
-    throw;
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, sc.key_a, sc.key_b, sc.idx_a, sc.idx_b,
+                                           (int)N, 0, bits > 0 ? bits : 1, s));
+  void* temp = sc.sort_temp(temp_bytes);
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, sc.key_a, sc.key_b, sc.idx_a, sc.idx_b,
+                                           (int)N, 0, bits > 0 ? bits : 1, s));
+  AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * d * N));
+  AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * N));
+  k_permute_nodes<<<bl, th, 0, s>>>(sc.nx_tmp, sc.idx_b, N, d, out->nx, out->perm);
+  AFS_CUDA(cudaGetLastError());
+  // column runs
+  int32_t* counts = sc.counts;
+  AFS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ncol, s));
+  k_column_counts<<<bl, th, 0, s>>>(sc.key_b, N, (uint64_t)n, counts);
+  AFS_CUDA(cudaGetLastError());
+  std::vector<int32_t> hc(ncol);
+  AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * ncol, cudaMemcpyDeviceToHost));
+  const int cap = chunk_cap_for(d, N);
+  std::vector<Chunk> ch;
+  int64_t pos = 0;
+  for (int64_t c = 0; c < ncol; ++c) {
+    for (int32_t o = 0; o < hc[c]; o += cap)
+      ch.push_back(Chunk{(int32_t)c, std::min(cap, hc[c] - o), pos + o, 0, 0});
+    pos += hc[c];
   }
-  cleanup();
+  out->N = N;
+  out->nchunks = (int64_t)ch.size();
+  out->chunk_cap = cap;
+  AFS_CUDA(cudaMalloc(&out->chunks, sizeof(Chunk) * std::max<size_t>(1, ch.size())));
+  AFS_CUDA(cudaMemcpy(out->chunks, ch.data(), sizeof(Chunk) * ch.size(), cudaMemcpyHostToDevice));
+  if (!ch.empty()) {
+    k_chunk_cell0<<<(unsigned)((ch.size() + 255) / 256), 256, 0, s>>>(
+        out->chunks, (int64_t)ch.size(), out->nx + (int64_t)(d - 1) * N, n);
+    AFS_CUDA(cudaGetLastError());
+  }
+  p->device_bytes += (int64_t)(sizeof(double) * d + sizeof(int32_t)) * N +
+                     (int64_t)sizeof(Chunk) * out->nchunks;
 }
 
 // ---- tensor-core layout (2-D windows, tc2d.cuh) -------------------------------------------
@@ -238,7 +260,8 @@ bool tc_eligible(int d, int m, int tab) {
   return !(e && e[0] == '0');
 }
 
-void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out) {
+void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                          BuildScratch& sc) {
   if (N >= (int64_t)INT32_MAX / 2) throw Error(AFS_ERR_VALIDATION, "at most 2^30-1 nodes per plan");
   if (w.d != 2) throw Error(AFS_ERR_VALIDATION, "tensor-core layout needs a 2-D window");
   if (p->n > (1 << 14)) throw Error(AFS_ERR_VALIDATION, "tensor-core layout needs n <= 16384");
@@ -247,78 +270,60 @@ void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t
   const cudaStream_t s = 0;
   int bits = 1;
   while ((1LL << bits) < nseg && bits < 63) ++bits;
-  double* nx_tmp = nullptr;
-  uint64_t *key_a = nullptr, *key_b = nullptr;
-  int32_t *idx_a = nullptr, *idx_b = nullptr, *counts = nullptr;
-  int64_t* starts = nullptr;
-  void* temp = nullptr;
-  size_t temp_bytes = 0;
-  auto cleanup = [&] {
-    cudaFree(nx_tmp); cudaFree(key_a); cudaFree(key_b); cudaFree(idx_a); cudaFree(idx_b);
-    cudaFree(counts); cudaFree(starts); cudaFree(temp);
-  };
-  try {
-    AFS_CUDA(cudaMalloc(&nx_tmp, sizeof(double) * 2 * std::max<int64_t>(N, 1)));
-    AFS_CUDA(cudaMalloc(&key_a, sizeof(uint64_t) * std::max<int64_t>(N, 1)));
-    AFS_CUDA(cudaMalloc(&key_b, sizeof(uint64_t) * std::max<int64_t>(N, 1)));
-    AFS_CUDA(cudaMalloc(&idx_a, sizeof(int32_t) * std::max<int64_t>(N, 1)));
-    AFS_CUDA(cudaMalloc(&idx_b, sizeof(int32_t) * std::max<int64_t>(N, 1)));
-    AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * nseg));
-    AFS_CUDA(cudaMemset(counts, 0, sizeof(int32_t) * nseg));
-    const int th = 256;
-    const int64_t bl = (N + th - 1) / th;
-    if (N > 0) {
-      k_prep_nodes_tc<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, nx_tmp, key_a, idx_a);
-      AFS_CUDA(cudaGetLastError());
-      AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key_a, key_b, idx_a, idx_b,
-                                               (int)N, 0, bits, s));
-      AFS_CUDA(cudaMalloc(&temp, temp_bytes));
-      AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_a, key_b, idx_a, idx_b,
-                                               (int)N, 0, bits, s));
-      k_segment_counts<<<bl, th, 0, s>>>(key_b, N, counts);
-      AFS_CUDA(cudaGetLastError());
-    }
-    std::vector<int32_t> hc(nseg);
-    AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost));
-    std::vector<int64_t> hs(2 * nseg);   // [seg_start | pad_start]
-    int64_t pos = 0, pad = 0;
-    for (int64_t k = 0; k < nseg; ++k) {
-      hs[k] = pos;
-      hs[nseg + k] = pad;
-      pos += hc[k];
-      pad += (hc[k] + 7) & ~7;
-    }
-    const int64_t ngroups = pad / 8;
-    const int64_t Npad = pad + 8 * kTcTailGroups;   // trailing empty groups (tc2d.cuh)
-    AFS_CUDA(cudaMalloc(&starts, sizeof(int64_t) * 2 * nseg));
-    AFS_CUDA(cudaMemcpy(starts, hs.data(), sizeof(int64_t) * 2 * nseg, cudaMemcpyHostToDevice));
-    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 2 * std::max<int64_t>(Npad, 1)));
-    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * std::max<int64_t>(Npad, 1)));
-    AFS_CUDA(cudaMalloc(&out->ghdr, sizeof(int32_t) * (Npad / 8)));
-    AFS_CUDA(cudaMemset(out->ghdr, 0, sizeof(int32_t) * (Npad / 8)));
-    AFS_CUDA(cudaMemset(out->nx, 0, sizeof(double) * 2 * Npad));
-    AFS_CUDA(cudaMemset(out->perm, 0xff, sizeof(int32_t) * Npad));   // -1: no node
-    if (N > 0) {
-      k_scatter_tc<<<bl, th, 0, s>>>(nx_tmp, idx_b, key_b, starts, starts + nseg, N, Npad, n, out->nx,
-                                     out->perm, out->ghdr);
-      AFS_CUDA(cudaGetLastError());
-      k_pad_tc<<<(unsigned)((nseg + th - 1) / th), th, 0, s>>>(counts, starts + nseg, nseg, Npad,
-                                                               out->nx, out->perm);
-      AFS_CUDA(cudaGetLastError());
-    }
-    out->N = Npad;
-    out->n_real = N;
-    out->ngroups = ngroups;
-    out->tc = true;
-    out->nchunks = 0;
-    out->chunk_cap = 0;
-    p->device_bytes += (int64_t)(sizeof(double) * 2 + sizeof(int32_t)) * Npad + (int64_t)sizeof(int32_t) * (Npad / 8);
-    AFS_CUDA(cudaDeviceSynchronize());
-  } catch (...) {
-    cleanup();
-    throw;
+  sc.reserve(N, 2);
+  sc.reserve_counts(nseg);
+  int32_t* counts = sc.counts;
+  int64_t* starts = sc.starts;
+  AFS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * nseg, s));
+  const int th = 256;
+  const int64_t bl = (N + th - 1) / th;
+  if (N > 0) {
+    k_prep_nodes_tc<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, sc.nx_tmp, sc.key_a, sc.idx_a);
+    AFS_CUDA(cudaGetLastError());
+    size_t temp_bytes = 0;
+    AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, sc.key_a, sc.key_b, sc.idx_a,
+                                             sc.idx_b, (int)N, 0, bits, s));
+    void* temp = sc.sort_temp(temp_bytes);
+    AFS_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, sc.key_a, sc.key_b, sc.idx_a,
+                                             sc.idx_b, (int)N, 0, bits, s));
+    k_segment_counts<<<bl, th, 0, s>>>(sc.key_b, N, counts);
+    AFS_CUDA(cudaGetLastError());
   }
-  cleanup();
+  std::vector<int32_t> hc(nseg);
+  AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> hs(2 * nseg);   // [seg_start | pad_start]
+  int64_t pos = 0, pad = 0;
+  for (int64_t k = 0; k < nseg; ++k) {
+    hs[k] = pos;
+    hs[nseg + k] = pad;
+    pos += hc[k];
+    pad += (hc[k] + 7) & ~7;
+  }
+  const int64_t ngroups = pad / 8;
+  const int64_t Npad = pad + 8 * kTcTailGroups;   // trailing empty groups (tc2d.cuh)
+  AFS_CUDA(cudaMemcpy(starts, hs.data(), sizeof(int64_t) * 2 * nseg, cudaMemcpyHostToDevice));
+  AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 2 * Npad));
+  AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * Npad));
+  AFS_CUDA(cudaMalloc(&out->ghdr, sizeof(int32_t) * (Npad / 8)));
+  AFS_CUDA(cudaMemsetAsync(out->ghdr, 0, sizeof(int32_t) * (Npad / 8), s));
+  AFS_CUDA(cudaMemsetAsync(out->nx, 0, sizeof(double) * 2 * Npad, s));
+  AFS_CUDA(cudaMemsetAsync(out->perm, 0xff, sizeof(int32_t) * Npad, s));   // -1: no node
+  if (N > 0) {
+    k_scatter_tc<<<bl, th, 0, s>>>(sc.nx_tmp, sc.idx_b, sc.key_b, starts, starts + nseg, N, Npad, n,
+                                   out->nx, out->perm, out->ghdr);
+    AFS_CUDA(cudaGetLastError());
+    k_pad_tc<<<(unsigned)((nseg + th - 1) / th), th, 0, s>>>(counts, starts + nseg, nseg, Npad,
+                                                             out->nx, out->perm);
+    AFS_CUDA(cudaGetLastError());
+  }
+  out->N = Npad;
+  out->n_real = N;
+  out->ngroups = ngroups;
+  out->tc = true;
+  out->nchunks = 0;
+  out->chunk_cap = 0;
+  p->device_bytes += (int64_t)(sizeof(double) * 2 + sizeof(int32_t)) * Npad +
+                     (int64_t)sizeof(int32_t) * (Npad / 8);
 }
 
 int kb_table_id(int M, int n) {

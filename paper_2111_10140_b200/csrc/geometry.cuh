@@ -50,10 +50,27 @@ struct SortedSide {
   __host__ __device__ const double* x1() const { return nx + N; }
 };
 
+// plan-build temporaries shared by all windows' sorts (grown on demand, freed by release)
+struct BuildScratch {
+  double* nx_tmp = nullptr;
+  uint64_t *key_a = nullptr, *key_b = nullptr;
+  int32_t *idx_a = nullptr, *idx_b = nullptr;
+  int64_t cap = 0;        // nodes the arrays above hold
+  void* temp = nullptr;   // CUB radix sort
+  size_t temp_bytes = 0;
+  int32_t* counts = nullptr;
+  int64_t* starts = nullptr;
+  int64_t counts_cap = 0;
+  void reserve(int64_t N, int d);
+  void reserve_counts(int64_t n);
+  void* sort_temp(size_t bytes);
+  void release();
+};
+
 void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
-                       SortedSide* out);
+                       SortedSide* out, BuildScratch& sc);
 void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N,
-                          SortedSide* out);
+                          SortedSide* out, BuildScratch& sc);
 bool tc_eligible(int d, int m, int tab);
 constexpr int kTcTailGroups = 16;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
 

@@ -187,10 +187,16 @@ class _Plan:
         descs = (_native.WindowDesc * len(feats))()
         self.n_windows = len(feats)
         self._keep = []
+        # upload first: the bbox reductions run on the device copy (exact, like numpy's)
+        Xd = X if not isinstance(X, np.ndarray) else torch.from_numpy(X)
+        Xd = Xd.to(self.device, non_blocking=False).contiguous()
+        Zd = None
+        if Z is not None:
+            Zd = (Z if not isinstance(Z, np.ndarray) else torch.from_numpy(Z)).to(self.device).contiguous()
         if scaling is None:
-            xlo, xhi = _all_columns_minmax(X)
+            xlo, xhi = _all_columns_minmax(Xd)
             if Z is not None:
-                zlo, zhi = _all_columns_minmax(Z)
+                zlo, zhi = _all_columns_minmax(Zd)
         for l, (w, eta) in enumerate(zip(feats, weights)):
             if scaling is not None:
                 # externally fixed (e.g. bbox all-reduced over point shards)
@@ -219,11 +225,6 @@ class _Plan:
             dsc.scale = scale
             dsc.weight = float(eta)
             dsc.multiplier = mult.ctypes.data_as(_native.c_double_p)
-        Xd = X if not isinstance(X, np.ndarray) else torch.from_numpy(X)
-        Xd = Xd.to(self.device, non_blocking=False).contiguous()
-        Zd = None
-        if Z is not None:
-            Zd = (Z if not isinstance(Z, np.ndarray) else torch.from_numpy(Z)).to(self.device).contiguous()
         desc = _native.PlanDesc()
         desc.device = self.device.index
         desc.n_windows = len(feats)

@@ -17,11 +17,17 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import numpy as np
+import scipy.fft as sfft
 from scipy.special import i0
 
 from .errors import NumericalError, ValidationError
 from .params import GaussianKernel, PeriodizationConfig
+
+
+_FFT_WORKERS = max(1, min(16, os.cpu_count() or 1))
 
 
 def _blend_poly(kernel: GaussianKernel, cfg: PeriodizationConfig) -> np.ndarray:
@@ -68,16 +74,36 @@ def regularize_kernel(kernel: GaussianKernel, config: PeriodizationConfig, dims:
         raise ValidationError(f"dimension must be 1..3, got {dims}")
     M = config.coeff_grid
     nn = M * config.coeff_oversample
-    ax = np.arange(-nn // 2, nn // 2) / nn
-    r2 = np.zeros((nn,) * dims)
-    for t in range(dims):
-        shape = [1] * dims
-        shape[t] = nn
-        r2 = r2 + (ax * ax).reshape(shape)
-    samples = periodized_profile(kernel, config)(np.sqrt(r2))
-    spec = np.fft.fftshift(np.fft.fftn(np.fft.ifftshift(samples)) / nn ** dims)
-    lo = nn // 2 - M // 2
-    return np.ascontiguousarray(spec[(slice(lo, lo + M),) * dims].real)
+    prof = periodized_profile(kernel, config)
+    if nn & (nn - 1) == 0:
+        # nn a power of two: (i/nn)^2 and their sums are exact, so r depends only on the
+        # integer s = sum_t i_t^2 -- evaluate the profile once per distinct s (<= d nn^2/4 + 1
+        # values instead of nn^d) and build the ifftshift-ed samples by lookup
+        i = sfft.ifftshift(np.arange(-nn // 2, nn // 2, dtype=np.int64))
+        sq = i * i
+        s2 = np.zeros((1,) * dims, dtype=np.int64)
+        for t in range(dims):
+            shape = [1] * dims
+            shape[t] = nn
+            s2 = s2 + sq.reshape(shape)
+        table = prof(np.sqrt(np.arange(dims * (nn // 2) ** 2 + 1) / float(nn * nn)))
+        shifted = table[s2]
+    else:
+        ax = np.arange(-nn // 2, nn // 2) / nn
+        r2 = np.zeros((nn,) * dims)
+        for t in range(dims):
+            shape = [1] * dims
+            shape[t] = nn
+            r2 = r2 + (ax * ax).reshape(shape)
+        shifted = sfft.ifftshift(prof(np.sqrt(r2)))
+    # scipy.fft (pocketfft) as the reference (fastsum.py:154-155); threads over the
+    # untransformed axes do not change any 1-D transform, so the result is bit-identical
+    spec = sfft.fftn(shifted, workers=_FFT_WORKERS)
+    # the centred M^d block of fftshift(spec) / nn^d, taken before shifting: frequencies
+    # -M/2 .. M/2-1 sit at indices k mod nn (elementwise the same division as the reference)
+    k = np.arange(-M // 2, M // 2) % nn
+    block = spec[np.ix_(*([k] * dims))] / nn ** dims
+    return np.ascontiguousarray(block.real)
 
 
 def kb_fourier(k, n: int, m: int, b: float):
