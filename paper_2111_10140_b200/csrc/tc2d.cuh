@@ -231,16 +231,18 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
   for (int gb = g0; gb < g1; gb += U) {
     cp_async_wait<1>();   // node data up to batch b + 2 and values of batch b have landed
     __syncwarp();
-    double x0[U], x1[U], prior[U][RG];
-    int j[U];
+    static_assert(U == 4, "the transposed quad reduction hands lane q the sums of group ug");
+    // after the reduction lane (slot, q) owns node slot of group ug = 2 (q & 1) + (q >> 1)
+    const int ug = 2 * (q & 1) + (q >> 1);
+    double x0[U], x1[U], prior[RG];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       x0[u] = R.x0[st][u * 8 + slot];
       x1[u] = R.x1[st][u * 8 + slot];
-      j[u] = R.perm[st][u * 8 + slot];
-#pragma unroll
-      for (int r = 0; r < RG; ++r) prior[u][r] = R.val[st][r][u * 8 + slot];
     }
+    const int j = R.perm[st][ug * 8 + slot];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) prior[r] = R.val[st][r][ug * 8 + slot];
     const Win wcur = wnext;
     const int st1 = st + 1 == D ? 0 : st + 1;
     const int st2 = st1 + 1 == D ? 0 : st1 + 1;
@@ -264,18 +266,26 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int r = 0; r < RG; ++r) {
+      // lane partials of the 4 groups, then a transposed reduction over the quad: 3 shuffles
+      // instead of 8, and every lane finishes one node
+      double sp[U];
 #pragma unroll
-      for (int r = 0; r < RG; ++r) {
+      for (int u = 0; u < U; ++u) {
         double t[2] = {0.0, 0.0};
         dmma884(t, fx[u][0], wcur.ga[u][r]);
         dmma884(t, fx[u][1], wcur.gc[u][r]);
-        double s = fma(t[1], fy[u][1], t[0] * fy[u][0]);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (q == 0 && j[u] >= 0 && r < nr)
-          out[r * ldo + j[u]] = __dadd_rn(prior[u][r], __dmul_rn(w.eta, s));
+        sp[u] = fma(t[1], fy[u][1], t[0] * fy[u][0]);
       }
+      const bool b0 = q & 1, b1 = (q >> 1) & 1;
+      // xor 1: keep groups {2 b0, 2 b0 + 1}
+      const double k0 = b0 ? sp[2] : sp[0], k1 = b0 ? sp[3] : sp[1];
+      const double g0 = b0 ? sp[0] : sp[2], g1 = b0 ? sp[1] : sp[3];
+      const double v0 = k0 + __shfl_xor_sync(0xffffffffu, g0, 1);
+      const double v1 = k1 + __shfl_xor_sync(0xffffffffu, g1, 1);
+      // xor 2: keep group 2 b0 + b1
+      const double sum = (b1 ? v1 : v0) + __shfl_xor_sync(0xffffffffu, b1 ? v0 : v1, 2);
+      if (j >= 0 && r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, sum));
     }
     st = st1;
   }
