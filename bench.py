@@ -252,8 +252,17 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # test hook for the multi-rank code path on a single-GPU box: AFS_BENCH_SHARE_GPU=1
+        # maps every rank onto the visible devices round-robin and uses gloo (host-staged
+        # all-reduce; no rank's kernels wait on another's).  Never used for reported numbers.
+        share = os.environ.get("AFS_BENCH_SHARE_GPU") == "1"
+        if share:
+            local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
