@@ -19,9 +19,10 @@ from .krr import (CgResult, KernelSystem, KrrConfig, KrrModel, cg_solve, decisio
                   load_model, model_from_dict, model_to_dict, predict, save_model)
 from .windowing import MisReport, ScalerStats, build_windows, mis_scores, zscore_apply, zscore_fit
 from .nfft import NfftPlan, nfft_adjoint, nfft_forward, validate_nodes
+from .harness import bench_mvm, direct_sum, ndft_adjoint_direct, ndft_direct
 
 __all__ = [
-    "AccuracyProfile", "AnovaKernelOperator", "CgResult", "DeviceError", "FastsumOperator",
+    "AccuracyProfile", "AnovaKernelOperator", "bench_mvm", "direct_sum", "ndft_adjoint_direct", "ndft_direct", "CgResult", "DeviceError", "FastsumOperator",
     "FreeWindowSet", "GaussianKernel", "GridSpec", "KernelSystem", "KrrConfig", "KrrModel",
     "MisReport", "NfftPlan", "NumericalError", "PROFILES", "PeriodizationConfig", "ScalerStats", "ShapeError",
     "ValidationError", "WindowSet", "anova_apply", "anova_build", "build_windows", "cg_solve",
