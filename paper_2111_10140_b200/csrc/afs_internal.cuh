@@ -113,13 +113,15 @@ struct afs_plan {
   std::vector<afs::GraphEntry> graphs;
   cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  // second branch of the spread / gather stages: windows alternate between the stage's
-  // stream and this one, so one window's tail overlaps the next window's kernel (spread
-  // grids are disjoint; the gather's odd windows accumulate into out2, added at the join)
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int stage_streams = 2;
-  double* out2 = nullptr;           // [max_rhs][Nt]
+  // extra branches of the spread / gather stages: window l runs on branch l % B (branch 0 =
+  // the stage's stream), so one window's tail overlaps the next windows' kernels (spread
+  // grids are disjoint; the gather's branch b > 0 accumulates into outx[b-1], added at the join)
+  static constexpr int kMaxBranches = 4;
+  cudaStream_t aux[kMaxBranches - 1] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[kMaxBranches - 1] = {nullptr, nullptr, nullptr};
+  int stage_streams = 0;            // 0: automatic (branch_count), else fixed 1..4
+  double* outx[kMaxBranches - 1] = {nullptr, nullptr, nullptr};   // [max_rhs][Nt] each
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};
@@ -141,7 +143,11 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
 void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
                    int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
 void make_twiddles(afs_plan* p);
-void ensure_aux_stream(afs_plan* p);
+void ensure_aux_streams(afs_plan* p);
+void fork_branches(afs_plan* p, int nb, cudaStream_t s);   // branches 1..nb-1 wait on s
+void join_branches(afs_plan* p, int nb, cudaStream_t s);   // s waits on branches 1..nb-1
+int spread_branches(const afs_plan* p);
+int gather_branches(const afs_plan* p, int R);
 
 // ---------------------------------------------------------------------------
 // grid accumulation of the spread

@@ -178,10 +178,12 @@ static void free_plan(afs_plan* p) {
   if (p->istream) cudaStreamDestroy(p->istream);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
-  if (p->aux) cudaStreamDestroy(p->aux);
-  cudaFree(p->out2);
+  for (int b = 0; b < afs_plan::kMaxBranches - 1; ++b) {
+    if (p->aux[b]) cudaStreamDestroy(p->aux[b]);
+    if (p->ev_join[b]) cudaEventDestroy(p->ev_join[b]);
+    cudaFree(p->outx[b]);
+  }
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
   for (SortedSide* s : p->src_side)
     if (s) { free_sorted_side(s); delete s; }
@@ -302,7 +304,8 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
     if (d->window_eval != 0 && d->window_eval != 1)
       throw Error(AFS_ERR_VALIDATION, "window_eval must be 0 (polynomial) or 1 (exact)");
     p->window_eval = d->window_eval;
-    if (const char* e = getenv("AFS_STAGE_STREAMS")) p->stage_streams = std::max(1, std::min(2, atoi(e)));
+    if (const char* e = getenv("AFS_STAGE_STREAMS"))
+      p->stage_streams = std::max(1, std::min(afs_plan::kMaxBranches, atoi(e)));
     {   // test hook: AFS_SPECTRAL_GENERIC=1 selects the generic line kernel for every n
       const char* g = getenv("AFS_SPECTRAL_GENERIC");
       p->fft_mode = (g && g[0] == '1') ? 1 : 0;

@@ -134,14 +134,30 @@ static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R
   return true;
 }
 
-__global__ void k_add_into(double* __restrict__ out, int64_t ldo, const double* __restrict__ add,
+// out += a0 (+ a1 (+ a2)): the extra branches' accumulators, in branch order
+__global__ void k_add_into(double* __restrict__ out, int64_t ldo, const double* __restrict__ a0,
+                           const double* __restrict__ a1, const double* __restrict__ a2, int na,
                            int64_t lda, int64_t N, int R) {
   const int64_t tot = N * R;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < tot;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = k / N, i = k - r * N;
-    out[r * ldo + i] += add[r * lda + i];
+    double v = out[r * ldo + i] + a0[r * lda + i];
+    if (na > 1) v += a1[r * lda + i];
+    if (na > 2) v += a2[r * lda + i];
+    out[r * ldo + i] = v;
   }
+}
+
+// Extra accumulators are read-modify-written at random (out[perm]); they only pay while all
+// of them stay L2-resident (C5: 4 x 8 MB; C3's 80 MB vectors measured slower with 2)
+int gather_branches(const afs_plan* p, int R) {
+  if (p->profiling || p->P < 2) return 1;
+  const int64_t bytes = p->Nt * R * (int64_t)sizeof(double);
+  int nb = p->stage_streams > 0 ? p->stage_streams : afs_plan::kMaxBranches;
+  nb = std::min(nb, p->P);
+  while (nb > 1 && nb * bytes > (48LL << 20)) --nb;
+  return nb;
 }
 
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
@@ -151,38 +167,35 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
     gather_v1(p, 0, p->P, out, ldo, R, s);
   } else {
     const bool timed = p->profiling && !p->wev_gather.empty();
-    // two branches (as the spread, spread.cu): odd windows accumulate into the plan's second
-    // output buffer on the aux stream, added at the join -- out = sum over even windows +
-    // sum over odd windows, each in window order (fixed, so run-to-run reproducible).  Only
-    // while both accumulators stay L2-resident: their random read-modify-writes otherwise
-    // compete for L2 and the overlap is lost (C3: 2 x 80 MB, measured slower)
-    const bool fork = !timed && p->stage_streams > 1 && p->P > 1 &&
-                      2 * p->Nt * R * (int64_t)sizeof(double) <= (64LL << 20);
-    if (fork) {
-      ensure_aux_stream(p);
-      if (!p->out2) {
-        AFS_CUDA(cudaMalloc(&p->out2, sizeof(double) * p->Nt * p->max_rhs));
-        p->device_bytes += sizeof(double) * p->Nt * p->max_rhs;
-      }
-      AFS_CUDA(cudaEventRecord(p->ev_fork, s));
-      AFS_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
-      AFS_CUDA(cudaMemsetAsync(p->out2, 0, sizeof(double) * p->Nt * R, p->aux));
+    // branches (as the spread, spread.cu): branch b > 0 accumulates its windows into the
+    // plan's output buffer outx[b-1], added at the join -- out = sum over branches of the
+    // windows' sums, each in window order (fixed, so run-to-run reproducible)
+    const int nb = timed ? 1 : gather_branches(p, R);
+    if (nb > 1) {
+      for (int b = 1; b < nb; ++b)
+        if (!p->outx[b - 1]) {
+          AFS_CUDA(cudaMalloc(&p->outx[b - 1], sizeof(double) * p->Nt * p->max_rhs));
+          p->device_bytes += sizeof(double) * p->Nt * p->max_rhs;
+        }
+      fork_branches(p, nb, s);
+      for (int b = 1; b < nb; ++b)
+        AFS_CUDA(cudaMemsetAsync(p->outx[b - 1], 0, sizeof(double) * p->Nt * R, p->aux[b - 1]));
     }
     for (int l = 0; l < p->P; ++l) {
       if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
-      const bool odd = fork && (l & 1);
-      const cudaStream_t sl = odd ? p->aux : s;
-      double* o = odd ? p->out2 : out;
-      const int64_t lo = odd ? p->Nt : ldo;
+      const int br = l % nb;
+      const cudaStream_t sl = br ? p->aux[br - 1] : s;
+      double* o = br ? p->outx[br - 1] : out;
+      const int64_t lo = br ? p->Nt : ldo;
       if (!gather_v2_window(p, l, o, lo, R, sl)) gather_v1(p, l, l + 1, o, lo, R, sl);
     }
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
-    if (fork) {
-      AFS_CUDA(cudaEventRecord(p->ev_join, p->aux));
-      AFS_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+    if (nb > 1) {
+      join_branches(p, nb, s);
       const int64_t tot = p->Nt * R;
       const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-      k_add_into<<<blocks, 256, 0, s>>>(out, ldo, p->out2, p->Nt, p->Nt, R);
+      k_add_into<<<blocks, 256, 0, s>>>(out, ldo, p->outx[0], p->outx[1], p->outx[2], nb - 1,
+                                        p->Nt, p->Nt, R);
     }
   }
   AFS_CUDA(cudaGetLastError());

@@ -164,11 +164,38 @@ __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stri
   grids[i] = (neg ? -mag : mag) * aux[2];
 }
 
-void ensure_aux_stream(afs_plan* p) {
-  if (p->aux) return;
-  AFS_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+void ensure_aux_streams(afs_plan* p) {
+  if (p->ev_fork) return;
+  for (int b = 0; b < afs_plan::kMaxBranches - 1; ++b) {
+    AFS_CUDA(cudaStreamCreateWithFlags(&p->aux[b], cudaStreamNonBlocking));
+    AFS_CUDA(cudaEventCreateWithFlags(&p->ev_join[b], cudaEventDisableTiming));
+  }
   AFS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-  AFS_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+}
+
+void fork_branches(afs_plan* p, int nb, cudaStream_t s) {
+  ensure_aux_streams(p);
+  AFS_CUDA(cudaEventRecord(p->ev_fork, s));
+  for (int b = 1; b < nb; ++b) AFS_CUDA(cudaStreamWaitEvent(p->aux[b - 1], p->ev_fork, 0));
+}
+
+void join_branches(afs_plan* p, int nb, cudaStream_t s) {
+  for (int b = 1; b < nb; ++b) {
+    AFS_CUDA(cudaEventRecord(p->ev_join[b - 1], p->aux[b - 1]));
+    AFS_CUDA(cudaStreamWaitEvent(s, p->ev_join[b - 1], 0));
+  }
+}
+
+// Large windows (C3: 0.2-1 ms kernels) gain most of the overlap from 2 branches; small ones
+// (C5 at N=1M: ~25 us kernels, tail-dominated) from 4.
+static int auto_branches(const afs_plan* p) {
+  if (p->stage_streams > 0) return p->stage_streams;
+  return p->Ns * (int64_t)p->P <= (int64_t)64 << 20 ? 4 : 2;
+}
+
+int spread_branches(const afs_plan* p) {
+  if (p->profiling || p->P < 2 || p->window_eval != 0) return 1;
+  return std::min(auto_branches(p), p->P);
 }
 
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
@@ -186,17 +213,14 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
     AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * cells, s));
   }
   const bool timed = p->profiling && !p->wev_spread.empty();
-  // two branches (not while timing windows): window l runs on branch l % 2
-  const bool fork = !timed && p->stage_streams > 1 && p->P > 1 && p->window_eval == 0;
-  if (fork) {
-    ensure_aux_stream(p);
-    AFS_CUDA(cudaEventRecord(p->ev_fork, s));
-    AFS_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
-  }
+  // branches (not while timing windows): window l runs on branch l % nb
+  const int nb = timed ? 1 : spread_branches(p);
+  if (nb > 1) fork_branches(p, nb, s);
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[l], s));
-    const cudaStream_t sl = (fork && (l & 1)) ? p->aux : s;
+    const int br = l % nb;
+    const cudaStream_t sl = br ? p->aux[br - 1] : s;
     if (spread_v2_window(p, l, alpha, lda, R, sl)) continue;
     switch (p->m) {
       case 1: launch_spread_m<1>(p, w, alpha, lda, R, sl); break;
@@ -209,10 +233,7 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
       default: launch_spread_m<8>(p, w, alpha, lda, R, sl); break;
     }
   }
-  if (fork) {
-    AFS_CUDA(cudaEventRecord(p->ev_join, p->aux));
-    AFS_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-  }
+  if (nb > 1) join_branches(p, nb, s);
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   if (det) {
     k_det_finalize<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
