@@ -25,6 +25,12 @@
 
 namespace afs {
 
+// __launch_bounds__ min blocks per SM of the team kernels: one right-hand side at a time fits
+// 4 blocks (<= 128 registers, no spills at m = 4; C3 3-D windows 4% faster than 3 blocks);
+// two at a time need their registers (capped they spill: C4 gather 6.8 -> 8.9 ms)
+// (m <= 4; larger cutoffs spill under the cap)
+template <int D, int MM, int RG>
+constexpr int v2_min_blocks() { return (D == 3 && RG == 1 && MM <= 4) ? 4 : 1; }
 #ifndef AFS_TEAM3
 #define AFS_TEAM3 32   // lanes per run for 3-D windows (power of two, 8..32)
 #endif
@@ -280,7 +286,7 @@ __device__ __forceinline__ int warp_max(int v) {
 // spread
 // ----------------------------------------------------------------------------
 template <int D, int MM, int RG, int TAB>
-__global__ void __launch_bounds__(128) k_spread_v2(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, v2_min_blocks<D, MM, RG>()) k_spread_v2(const SortedSide sv, const Window w, int n,
                                                    const PolyTable T,
                                                    const double* __restrict__ alpha, int64_t lda,
                                                    int nr, double* __restrict__ grid,
@@ -397,7 +403,7 @@ struct Red {
 };
 
 template <int D, int MM, int RG, int TAB>
-__global__ void __launch_bounds__(128) k_gather_v2(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, v2_min_blocks<D, MM, RG>()) k_gather_v2(const SortedSide sv, const Window w, int n,
                                                    const PolyTable T,
                                                    const double* __restrict__ grid,
                                                    int64_t rhs_stride, int nr,
