@@ -95,6 +95,8 @@ typedef struct afs_plan_info {
   int32_t grid;
   int64_t n_sources;
   int64_t n_targets;
+  /* kernels one afs_apply launches: counted from its captured CUDA graph once one exists
+   * (second apply with the same buffers), a plan-time estimate before */
   int32_t kernel_launches_per_apply;
 } afs_plan_info;
 

@@ -87,6 +87,19 @@ static bool apply_graph(afs_plan* p, const double* alpha, int64_t lda, double* o
     throw;
   }
   AFS_CUDA(cudaStreamEndCapture(s, &graph));
+  {   // the exact kernel count of one apply (afs_plan_info.kernel_launches_per_apply)
+    size_t nn = 0;
+    AFS_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) AFS_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    int kernels = 0;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      AFS_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    p->launches_per_apply = kernels;
+  }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -319,7 +332,7 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       BuildScratch sc;   // sort temporaries shared by all windows
       try {
         for (int l = 0; l < p->P; ++l) {
-          const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab);
+          const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
           auto build = tc ? build_sorted_side_tc : build_sorted_side;
           p->src_side[l] = new SortedSide();
           build(p, p->win[l], p->src, p->Ns, p->src_side[l], sc);

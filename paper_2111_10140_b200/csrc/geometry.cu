@@ -254,8 +254,10 @@ __global__ void k_pad_tc(const int32_t* __restrict__ counts, const int64_t* __re
   }
 }
 
-bool tc_eligible(int d, int m, int tab) {
-  if (d != 2 || m != 4 || tab == 0) return false;
+bool tc_eligible(int d, int m, int tab, int n, int64_t N) {
+  // 8-offset stencils (m = 4) on a compile-time table; 14-bit cells in the group header;
+  // int32 node indices in the kernels
+  if (d != 2 || m != 4 || tab == 0 || n > (1 << 14) || N >= (int64_t)INT32_MAX / 2) return false;
   const char* e = getenv("AFS_TC");   // A/B hook: AFS_TC=0 keeps the FMA kernels
   return !(e && e[0] == '0');
 }

@@ -71,7 +71,7 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
                        SortedSide* out, BuildScratch& sc);
 void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N,
                           SortedSide* out, BuildScratch& sc);
-bool tc_eligible(int d, int m, int tab);
+bool tc_eligible(int d, int m, int tab, int n, int64_t N);
 constexpr int kTcTailGroups = 16;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
 
 // group header of the tensor-core layout: wrapped base cells and reflection classes
