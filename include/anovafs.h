@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define AFS_ABI_VERSION 1
+#define AFS_ABI_VERSION 2
 
 enum afs_status {
   AFS_OK = 0,
@@ -98,6 +98,8 @@ typedef struct afs_plan_info {
   /* kernels one afs_apply launches: counted from its captured CUDA graph once one exists
    * (second apply with the same buffers), a plan-time estimate before */
   int32_t kernel_launches_per_apply;
+  /* windows whose (source-side) nodes run on the fp64 tensor-core kernels (ABI 2) */
+  int32_t tensor_core_windows;
 } afs_plan_info;
 
 int afs_abi_version(void);

@@ -60,6 +60,7 @@ class PlanInfo(ctypes.Structure):
         ("n_sources", ctypes.c_int64),
         ("n_targets", ctypes.c_int64),
         ("kernel_launches_per_apply", ctypes.c_int32),
+        ("tensor_core_windows", ctypes.c_int32),
     ]
 
 
@@ -116,7 +117,7 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.afs_abi_version() != 1:
+        if lib.afs_abi_version() != 2:
             raise ImportError("libanovafs ABI version mismatch")
         _lib = lib
         return lib

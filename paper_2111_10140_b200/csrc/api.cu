@@ -332,13 +332,21 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       BuildScratch sc;   // sort temporaries shared by all windows
       try {
         for (int l = 0; l < p->P; ++l) {
-          const bool tc = tc_eligible(p->win[l].d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
-          auto build = tc ? build_sorted_side_tc : build_sorted_side;
+          const Window& w = p->win[l];
+          const bool tc = tc_eligible(w.d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
+          // dense 3-D windows take the tensor-core layout when padding the half-cells to groups
+          // of 8 adds at most 15% nodes (tc3d.cuh); sparse ones keep the team kernels
+          const bool tc3 = tc3_eligible(w.d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
+          auto build = [&](const double* X, int64_t N, SortedSide* side) {
+            if (tc) return build_sorted_side_tc(p, w, X, N, side, sc);
+            if (tc3 && build_sorted_side_tc3(p, w, X, N, side, sc, 0.15)) return;
+            build_sorted_side(p, w, X, N, side, sc);
+          };
           p->src_side[l] = new SortedSide();
-          build(p, p->win[l], p->src, p->Ns, p->src_side[l], sc);
+          build(p->src, p->Ns, p->src_side[l]);
           if (p->has_targets) {
             p->tgt_side[l] = new SortedSide();
-            build(p, p->win[l], p->tgt, p->Nt, p->tgt_side[l], sc);
+            build(p->tgt, p->Nt, p->tgt_side[l]);
           }
         }
         AFS_CUDA(cudaDeviceSynchronize());
@@ -384,6 +392,9 @@ int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info) {
     info->n_sources = plan->Ns;
     info->n_targets = plan->Nt;
     info->kernel_launches_per_apply = plan->launches_per_apply;
+    int tcw = 0;
+    for (const afs::SortedSide* sv : plan->src_side) tcw += (sv && sv->tc) ? 1 : 0;
+    info->tensor_core_windows = tcw;
   });
 }
 

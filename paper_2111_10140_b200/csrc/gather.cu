@@ -10,6 +10,7 @@
 #include "afs_internal.cuh"
 #include "sliding.cuh"
 #include "tc2d.cuh"
+#include "tc3d.cuh"
 
 namespace afs {
 
@@ -113,6 +114,8 @@ static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R
   if (p->window_eval != 0) return false;
   const Window& w = p->win[l];
   const SortedSide& sv = p->has_targets ? *p->tgt_side[l] : *p->src_side[l];
+  if (sv.tc && w.d == 3)
+    return launch_gather_tc3(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);
   if (sv.tc) return launch_gather_tc(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);
   const int rg = v2_rhs_group(w.d, p->m, R);
   if (rg < 1) return false;

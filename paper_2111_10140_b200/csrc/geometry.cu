@@ -328,6 +328,179 @@ void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t
                      (int64_t)sizeof(int32_t) * (Npad / 8);
 }
 
+// ---- tensor-core layout for dense 3-D windows (tc3d.cuh) ------------------------------------
+// Same half-cell idea as the 2-D layout, over (2n)^3 keys; segments come from a device
+// run-length pass over the sorted keys (no host table of (2n)^3 counts).
+__global__ void k_prep_nodes_tc3(const double* __restrict__ X, int64_t N, int dtot, Window w, int n,
+                                 double* __restrict__ nx_out, uint64_t* __restrict__ key,
+                                 int32_t* __restrict__ idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  uint64_t k = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const double xs = scaled_coord(X[j * dtot + w.feat[t]], w.center[t], w.scale);
+    const double nx = __dmul_rn((double)n, xs);   // nfft.py:170
+    nx_out[t * N + j] = nx;
+    const double fl = floor(nx);
+    long long u = (long long)fl % n;
+    if (u < 0) u += n;
+    const int c = (nx - fl) > 0.5 ? 1 : 0;
+    k = k * (uint64_t)(2 * n) + (uint64_t)(2 * u + c);
+  }
+  key[j] = k;
+  idx[j] = (int32_t)j;
+}
+
+// run heads of the sorted keys
+__global__ void k_run_heads(const uint64_t* __restrict__ key, int64_t N, int32_t* __restrict__ head) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  head[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_minus1(int32_t* __restrict__ v, int64_t N) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) v[i] -= 1;
+}
+
+// each run's first node records the run's start, its last node the run's end (exclusive)
+__global__ void k_run_bounds(const int32_t* __restrict__ run_id, int64_t N, int32_t* __restrict__ start,
+                             int32_t* __restrict__ len) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t r = run_id[i];
+  if (i == 0 || run_id[i - 1] != r) start[r] = (int32_t)i;
+  if (i == N - 1 || run_id[i + 1] != r) len[r] = (int32_t)(i + 1);
+}
+
+// end -> length padded to a multiple of 8
+__global__ void k_run_pad(const int32_t* __restrict__ start, int32_t* __restrict__ len, int64_t nruns) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nruns) return;
+  const int32_t c = len[r] - start[r];
+  len[r] = (c + 7) & ~7;
+}
+
+__global__ void k_scatter_tc3(const double* __restrict__ nx_in, const int32_t* __restrict__ idx,
+                              const int32_t* __restrict__ run_id, const int32_t* __restrict__ start,
+                              const int64_t* __restrict__ pad_start, int64_t N, int64_t Npad, int n,
+                              double* __restrict__ x_out, int32_t* __restrict__ perm,
+                              uint64_t* __restrict__ ghdr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t r = run_id[i];
+  const int64_t dst = pad_start[r] + (i - start[r]);
+  const int32_t j = idx[i];
+  perm[dst] = j;
+  uint64_t h = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const double nx = nx_in[t * N + j];
+    const double fl = floor(nx);
+    const double f = nx - fl;   // exact
+    const int c = f > 0.5 ? 1 : 0;
+    long long uu = (long long)fl % n;
+    const uint64_t u = (uint64_t)(uu < 0 ? uu + n : uu);
+    x_out[t * Npad + dst] = (c ? __dsub_rn(1.0, f) : f) - 0.25;   // as poly_weights
+    h |= (u << (16 * t)) | ((uint64_t)c << (48 + t));
+  }
+  if ((dst & 7) == 0) ghdr[dst >> 3] = h;
+}
+
+// Opt-in (AFS_TC3=1): measured on C4's clusters the tensor-core 3-D kernels are 6% faster than
+// the team kernels at N = 1e8 (110 vs 117 ms/matvec, R = 8) but slower at N = 1e7 (19.7 vs
+// 14.6 ms: the spread's per-half-cell flushes of 512 cells x R dominate shorter segments).
+bool tc3_eligible(int d, int m, int tab, int n, int64_t N) {
+  if (d != 3 || m != 4 || tab == 0 || n > 1024 || N < 8 || N >= (int64_t)INT32_MAX / 2) return false;
+  const char* e = getenv("AFS_TC");
+  if (e && e[0] == '0') return false;
+  const char* e3 = getenv("AFS_TC3");
+  return e3 && e3[0] == '1';
+}
+
+bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                           BuildScratch& sc, double max_padding) {
+  const int n = p->n;
+  const cudaStream_t s = 0;
+  int bits = 1;
+  {
+    const long double keys = (long double)(2 * n) * (2 * n) * (2 * n);
+    while ((long double)(1ULL << bits) < keys && bits < 63) ++bits;
+  }
+  sc.reserve(N, 3);
+  const int th = 256;
+  const int64_t bl = (N + th - 1) / th;
+  k_prep_nodes_tc3<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, sc.nx_tmp, sc.key_a, sc.idx_a);
+  AFS_CUDA(cudaGetLastError());
+  size_t temp_bytes = 0;
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, sc.key_a, sc.key_b, sc.idx_a, sc.idx_b,
+                                           (int)N, 0, bits, s));
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(sc.sort_temp(temp_bytes), temp_bytes, sc.key_a, sc.key_b,
+                                           sc.idx_a, sc.idx_b, (int)N, 0, bits, s));
+  // run ids: key_a is free now (sorted keys live in key_b); reuse it as two int32 arrays
+  int32_t* head = reinterpret_cast<int32_t*>(sc.key_a);
+  int32_t* run_id = head + N;
+  k_run_heads<<<bl, th, 0, s>>>(sc.key_b, N, head);
+  AFS_CUDA(cudaGetLastError());
+  temp_bytes = 0;
+  AFS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, head, run_id, (int)N, s));
+  AFS_CUDA(cub::DeviceScan::InclusiveSum(sc.sort_temp(temp_bytes), temp_bytes, head, run_id, (int)N, s));
+  int32_t nruns = 0;
+  AFS_CUDA(cudaMemcpy(&nruns, run_id + N - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  k_minus1<<<bl, th, 0, s>>>(run_id, N);   // the inclusive scan counts runs from 1
+  AFS_CUDA(cudaGetLastError());
+  int32_t *start = nullptr, *padded = nullptr;
+  int64_t* pad_start = nullptr;
+  auto cleanup = [&] { cudaFree(start); cudaFree(padded); cudaFree(pad_start); };
+  try {
+    AFS_CUDA(cudaMalloc(&start, sizeof(int32_t) * nruns));
+    AFS_CUDA(cudaMalloc(&padded, sizeof(int32_t) * nruns));
+    AFS_CUDA(cudaMalloc(&pad_start, sizeof(int64_t) * (nruns + 1)));
+    k_run_bounds<<<bl, th, 0, s>>>(run_id, N, start, padded);
+    AFS_CUDA(cudaGetLastError());
+    k_run_pad<<<(unsigned)((nruns + th - 1) / th), th, 0, s>>>(start, padded, nruns);
+    AFS_CUDA(cudaGetLastError());
+    // pad_start = exclusive scan of padded lengths (64-bit), pad_start[nruns] = total
+    AFS_CUDA(cudaMemsetAsync(pad_start, 0, sizeof(int64_t), s));
+    temp_bytes = 0;
+    AFS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, padded, pad_start + 1, (int)nruns, s));
+    AFS_CUDA(cub::DeviceScan::InclusiveSum(sc.sort_temp(temp_bytes), temp_bytes, padded, pad_start + 1,
+                                           (int)nruns, s));
+    int64_t total = 0;
+    AFS_CUDA(cudaMemcpy(&total, pad_start + nruns, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if ((double)(total - N) > max_padding * (double)N) {   // sparse: the FMA kernels win
+      cleanup();
+      return false;
+    }
+    const int64_t ngroups = total / 8;
+    const int64_t Npad = total + 8 * kTcTailGroups;
+    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 3 * Npad));
+    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * Npad));
+    AFS_CUDA(cudaMalloc(&out->ghdr64, sizeof(uint64_t) * (Npad / 8)));
+    AFS_CUDA(cudaMemsetAsync(out->ghdr64, 0, sizeof(uint64_t) * (Npad / 8), s));
+    AFS_CUDA(cudaMemsetAsync(out->nx, 0, sizeof(double) * 3 * Npad, s));
+    AFS_CUDA(cudaMemsetAsync(out->perm, 0xff, sizeof(int32_t) * Npad, s));   // -1: no node
+    k_scatter_tc3<<<bl, th, 0, s>>>(sc.nx_tmp, sc.idx_b, run_id, start, pad_start, N, Npad, n,
+                                    out->nx, out->perm, out->ghdr64);
+    AFS_CUDA(cudaGetLastError());
+    out->N = Npad;
+    out->n_real = N;
+    out->ngroups = ngroups;
+    out->tc = true;
+    out->nchunks = 0;
+    out->chunk_cap = 0;
+    p->device_bytes += (int64_t)(sizeof(double) * 3 + sizeof(int32_t)) * Npad +
+                       (int64_t)sizeof(uint64_t) * (Npad / 8);
+    AFS_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  return true;
+}
+
 int kb_table_id(int M, int n) {
   if (n == 2 * M) return 1;
   if (2 * n == 3 * M) return 2;
@@ -336,6 +509,7 @@ int kb_table_id(int M, int n) {
 
 void free_sorted_side(SortedSide* s) {
   cudaFree(s->ghdr);
+  cudaFree(s->ghdr64);
   cudaFree(s->nx);
   cudaFree(s->perm);
   cudaFree(s->chunks);

@@ -45,9 +45,11 @@ struct SortedSide {
   bool tc = false;
   int64_t n_real = 0;
   int32_t* ghdr = nullptr;
+  uint64_t* ghdr64 = nullptr;   // 3-D layout: u0 | u1 << 16 | u2 << 32 | c_t << (48 + t)
   int64_t ngroups = 0;   // groups of 8 holding nodes; N / 8 - ngroups >= kTcTailGroups empty ones follow
   __host__ __device__ const double* x0() const { return nx; }
   __host__ __device__ const double* x1() const { return nx + N; }
+  __host__ __device__ const double* x2() const { return nx + 2 * N; }
 };
 
 // plan-build temporaries shared by all windows' sorts (grown on demand, freed by release)
@@ -72,6 +74,11 @@ void build_sorted_side(afs_plan* p, const Window& w, const double* X, int64_t N,
 void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N,
                           SortedSide* out, BuildScratch& sc);
 bool tc_eligible(int d, int m, int tab, int n, int64_t N);
+bool tc3_eligible(int d, int m, int tab, int n, int64_t N);
+// dense 3-D windows: the tensor-core layout, or false (nothing built) when padding the
+// half-cells to groups of 8 would add more than max_padding * N nodes
+bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                           BuildScratch& sc, double max_padding);
 constexpr int kTcTailGroups = 16;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
 
 // group header of the tensor-core layout: wrapped base cells and reflection classes

@@ -9,6 +9,7 @@
 #include "afs_internal.cuh"
 #include "sliding.cuh"
 #include "tc2d.cuh"
+#include "tc3d.cuh"
 
 namespace afs {
 
@@ -85,6 +86,8 @@ static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t ld
   if (p->window_eval != 0) return false;
   const Window& w = p->win[l];
   const SortedSide& sv = *p->src_side[l];
+  if (sv.tc && w.d == 3)
+    return launch_spread_tc3(sv, w, p->n, p->kb_tab, alpha, lda, R, p->grids, p->grid_total, s);
   if (sv.tc) return launch_spread_tc(sv, w, p->n, p->kb_tab, alpha, lda, R, p->grids, p->grid_total, s);
   const int rg = v2_rhs_group(w.d, p->m, R);
   if (rg < 1) return false;
