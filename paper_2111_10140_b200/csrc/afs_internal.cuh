@@ -60,6 +60,12 @@ struct GraphEntry {
   cudaGraphExec_t exec;
 };
 
+struct CgGraph {
+  cudaGraphExec_t exec = nullptr;
+  double* x = nullptr;   // key: the solution buffer and the shift baked into the graph
+  double beta = 0.0;
+};
+
 struct CgScratch {
   double* r = nullptr;
   double* p = nullptr;
@@ -68,6 +74,7 @@ struct CgScratch {
   double* scalars = nullptr;   // device scalars (see cg.cu)
   double* host_scalars = nullptr;  // pinned
   int64_t n = 0;
+  CgGraph graph;   // whole-solve graph: a device-side while loop over the iteration body
 };
 
 }  // namespace afs
@@ -140,6 +147,10 @@ void spectral_all(afs_plan* p, int R, cudaStream_t s, int mode = 0);   // 0 fuse
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
 void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
                 int R, cudaStream_t s);
+// the three stages on stream s, no graph (capturable once a warm-up apply ran: allocations
+// and one-time kernel attributes happen on first use)
+void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                  int R, cudaStream_t s);
 void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
                    int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
 void make_twiddles(afs_plan* p);

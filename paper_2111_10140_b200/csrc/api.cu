@@ -49,8 +49,8 @@ void make_twiddles(afs_plan* p) {
   p->device_bytes += sizeof(double2) * p->n;
 }
 
-static void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
-                         int R, cudaStream_t s) {
+void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                  int R, cudaStream_t s) {
   spread_all(p, alpha, lda, R, s);
   spectral_all(p, R, s);
   gather_all(p, out, ldo, R, s);

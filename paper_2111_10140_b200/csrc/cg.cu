@@ -6,9 +6,13 @@
 //         stop if sqrt(rs_new) <= tol ||b||;  p = r + (rs_new/rs) p
 // Vector updates are fused with the dot products they feed; reductions are
 // two-stage with a fixed grid, so results are run-to-run deterministic.
-// One 32-byte host read-back per iteration keeps the stopping rule (and the
-// iteration count) identical to the reference's host loop.
+// The default solve is one CUDA graph: a conditional WHILE node whose body is the captured
+// matvec + the update kernels + a one-thread decision kernel that applies the reference's
+// stopping rule and breakdown checks on device scalars (cudaGraphSetConditional), so the
+// iteration count is the reference's with no host round trip per iteration.  The host loop
+// (one 32-byte read-back per iteration) remains as the fallback (AFS_CG_GRAPH=0).
 #include <cmath>
+#include <cstdlib>
 
 #include "afs_internal.cuh"
 
@@ -102,22 +106,171 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_dir(double* __restrict__ p,
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
+// ---- device-side loop (graph conditional node) -------------------------------------------
+// ds: [0] rs  [1] pAp  [2] rs_new  [3] non-finite flag  [4] iterations  [5] status
+//     [6] tol * ||b||  [7] maxiter  [8] rs_new / rs (direction update)
+enum : int { kCgRunning = 0, kCgConverged = 1, kCgMaxiter = 2, kCgBadAp = -1, kCgBadCurv = -2,
+             kCgBadRes = -3 };
+
+__global__ void __launch_bounds__(kRedThreads) k_cg_update_dev(double* __restrict__ x,
+                                                              double* __restrict__ r,
+                                                              const double* __restrict__ p,
+                                                              const double* __restrict__ ap,
+                                                              const double* __restrict__ ds,
+                                                              int64_t n, double* __restrict__ partial) {
+  const double step = ds[0] / ds[1];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(step, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(step, ap[i]));
+    r[i] = ri;
+    v += ri * ri;
+  }
+  v = block_sum(v);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+}
+
+// the host loop's checks, in its order (krr.py:93-106)
+__global__ void k_cg_decide(double* ds, cudaGraphConditionalHandle h) {
+  const double it = ds[4] + 1.0;
+  ds[4] = it;
+  const double pAp = ds[1], rs_new = ds[2];
+  int status = kCgRunning;
+  if (ds[3] != 0.0) status = kCgBadAp;
+  else if (!isfinite(pAp) || pAp <= 0.0) status = kCgBadCurv;
+  else if (!isfinite(rs_new)) status = kCgBadRes;
+  else if (sqrt(rs_new) <= ds[6]) status = kCgConverged;
+  else if (it >= ds[7]) status = kCgMaxiter;
+  if (status >= 0) {
+    ds[8] = rs_new / ds[0];
+    ds[0] = rs_new;
+  }
+  ds[5] = (double)status;
+  cudaGraphSetConditional(h, status == kCgRunning ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_cg_dir_dev(double* __restrict__ p,
+                                                           const double* __restrict__ r,
+                                                           const double* __restrict__ ds, int64_t n) {
+  const double beta = ds[8];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+}
+
 static void ensure_cg(afs_plan* pl) {
   CgScratch& c = pl->cg;
   if (c.n == pl->Ns) return;
   if (c.r) {
     cudaFree(c.r); cudaFree(c.p); cudaFree(c.ap); cudaFree(c.partial); cudaFree(c.scalars);
     cudaFreeHost(c.host_scalars);
+    if (c.graph.exec) cudaGraphExecDestroy(c.graph.exec);
+    c.graph = CgGraph{};
   }
   const size_t bytes = sizeof(double) * pl->Ns;
   AFS_CUDA(cudaMalloc(&c.r, bytes));
   AFS_CUDA(cudaMalloc(&c.p, bytes));
   AFS_CUDA(cudaMalloc(&c.ap, bytes));
   AFS_CUDA(cudaMalloc(&c.partial, sizeof(double) * kRedBlocks));
-  AFS_CUDA(cudaMalloc(&c.scalars, sizeof(double) * 8));
-  AFS_CUDA(cudaMallocHost(&c.host_scalars, sizeof(double) * 8));
+  AFS_CUDA(cudaMalloc(&c.scalars, sizeof(double) * 16));
+  AFS_CUDA(cudaMallocHost(&c.host_scalars, sizeof(double) * 16));
   c.n = pl->Ns;
   pl->device_bytes += 3 * bytes + sizeof(double) * (kRedBlocks + 8);
+}
+
+// Builds (or reuses) the whole-loop graph for solution buffer x and shift beta.  Returns
+// false when conditional graph nodes are unavailable (then the host loop runs).
+static bool cg_graph(afs_plan* pl, const double* b, double* x, double beta, cudaStream_t s) {
+  CgScratch& c = pl->cg;
+  if (c.graph.exec && c.graph.x == x && c.graph.beta == beta) return true;
+  if (c.graph.exec) {
+    cudaGraphExecDestroy(c.graph.exec);
+    c.graph = CgGraph{};
+  }
+  const int64_t n = pl->Ns;
+  double* ds = c.scalars;
+  // warm-up: one eager matvec performs the stages' first-use allocations and kernel
+  // attributes, which must not happen inside the capture (overwrites Ap only)
+  apply_stages(pl, b, n, c.ap, n, 1, s);
+  cudaGraph_t g = nullptr;
+  AFS_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  cudaGraphNodeParams prm = {};
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e == cudaSuccess) {
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &prm);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    return false;
+  }
+  cudaGraph_t body = prm.conditional.phGraph_out[0];
+  AFS_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  try {
+    apply_stages(pl, c.p, n, c.ap, n, 1, s);
+    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, beta, n, c.partial, ds + 3);
+    k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 1);
+    k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.ap, ds, n, c.partial);
+    k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 2);
+    k_cg_decide<<<1, 1, 0, s>>>(ds, h);
+    k_cg_dir_dev<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.r, ds, n);
+  } catch (...) {
+    cudaStreamEndCapture(s, &body);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  AFS_CUDA(cudaStreamEndCapture(s, &body));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  AFS_CUDA(e);
+  c.graph.exec = exec;
+  c.graph.x = x;
+  c.graph.beta = beta;
+  return true;
+}
+
+static void cg_solve_graph(afs_plan* pl, const double* b, double* x, double beta, double tol,
+                           int maxiter, int* iters, double* resid, int* conv, cudaStream_t s,
+                           double bnorm) {
+  CgScratch& c = pl->cg;
+  double* hs = c.host_scalars;
+  double* ds = c.scalars;
+  const int64_t n = pl->Ns;
+  // ds[0] = rs = ||b||^2 is in place; iteration state and limits
+  hs[3] = 0.0;
+  hs[4] = 0.0;
+  hs[5] = 0.0;
+  hs[6] = tol * bnorm;
+  hs[7] = (double)maxiter;
+  AFS_CUDA(cudaMemcpyAsync(ds + 3, hs + 3, 5 * sizeof(double), cudaMemcpyHostToDevice, s));
+  AFS_CUDA(cudaMemcpyAsync(c.r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  AFS_CUDA(cudaMemcpyAsync(c.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  AFS_CUDA(cudaGraphLaunch(c.graph.exec, s));
+  AFS_CUDA(cudaMemcpyAsync(hs, ds, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  AFS_CUDA(cudaStreamSynchronize(s));
+  const int it = (int)hs[4];
+  const int status = (int)hs[5];
+  *iters = it;
+  if (status == kCgBadAp)
+    throw Error(AFS_ERR_NUMERICAL, "CG breakdown: non-finite operator output at iteration " +
+                                       std::to_string(it));
+  if (status == kCgBadCurv) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "CG breakdown: non-positive curvature %.3e at iteration %d", hs[1], it);
+    throw Error(AFS_ERR_NUMERICAL, buf);
+  }
+  if (status == kCgBadRes)
+    throw Error(AFS_ERR_NUMERICAL, "CG breakdown: non-finite residual at iteration " + std::to_string(it));
+  *resid = std::sqrt(hs[0]) / bnorm;
+  *conv = status == kCgConverged ? 1 : 0;
 }
 
 void cg_solve_impl(afs_plan* pl, const double* b, double* x, double beta, double tol,
@@ -142,6 +295,22 @@ void cg_solve_impl(afs_plan* pl, const double* b, double* x, double beta, double
   *resid = 0.0;
   *conv = 1;
   if (bnorm == 0.0) return;
+  {   // whole solve as one graph on the plan's capturable stream, ordered with the caller's
+    const char* e = getenv("AFS_CG_GRAPH");
+    if (!(e && e[0] == '0')) {
+      if (!pl->istream) {
+        AFS_CUDA(cudaStreamCreateWithFlags(&pl->istream, cudaStreamNonBlocking));
+        AFS_CUDA(cudaEventCreateWithFlags(&pl->ev_in, cudaEventDisableTiming));
+        AFS_CUDA(cudaEventCreateWithFlags(&pl->ev_out, cudaEventDisableTiming));
+      }
+      AFS_CUDA(cudaEventRecord(pl->ev_in, s));
+      AFS_CUDA(cudaStreamWaitEvent(pl->istream, pl->ev_in, 0));
+      if (cg_graph(pl, b, x, beta, pl->istream)) {
+        cg_solve_graph(pl, b, x, beta, tol, maxiter, iters, resid, conv, pl->istream, bnorm);
+        return;   // synchronised with the host; nothing left on either stream
+      }
+    }
+  }
   AFS_CUDA(cudaMemcpyAsync(c.r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   AFS_CUDA(cudaMemcpyAsync(c.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   double rs = hs[0];
