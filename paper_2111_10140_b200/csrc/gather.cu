@@ -117,7 +117,7 @@ static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R
   if (sv.tc && w.d == 3)
     return launch_gather_tc3(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);
   if (sv.tc) return launch_gather_tc(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);
-  const int rg = v2_rhs_group(w.d, p->m, R);
+  const int rg = v2_rhs_group(w.d, p->m, R, false);
   if (rg < 1) return false;
   for (int r0 = 0; r0 < R; r0 += rg) {
     const int nr = std::min(rg, R - r0);

@@ -563,6 +563,6 @@ template <int D>
 bool launch_gather_v2(const SortedSide& sv, const Window& w, int n, int m, int tab, const PolyTable& T,
                       const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                       cudaStream_t s);
-int v2_rhs_group(int D, int m, int R);
+int v2_rhs_group(int D, int m, int R, bool spread);   // right-hand sides per pass
 
 }  // namespace afs

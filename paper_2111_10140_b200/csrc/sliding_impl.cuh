@@ -76,6 +76,12 @@ template <int D, int MM, int TAB>
 static bool spread_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* alpha, int64_t lda, int nr, double* grid, int64_t rs,
                        cudaStream_t s) {
+  if constexpr (D == 3 && MM == 4 && TAB != 0 && Fits<D, MM, 4>::value) {
+    if (nr >= 3) {   // v2_rhs_group: RHS groups of 4 for the 3-D spread
+      run_spread_v2<D, MM, 4, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
+      return true;
+    }
+  }
   if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
     if (nr >= 2) {
       run_spread_solo<D, MM, 2, TAB>(sv, w, n, T, alpha, lda, nr, grid, rs, s);
@@ -116,6 +122,7 @@ template <int D, int MM, int TAB>
 static bool gather_tab(const SortedSide& sv, const Window& w, int n, const PolyTable& T,
                        const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                        cudaStream_t s) {
+
   if constexpr (SoloFits<D, MM, 2>::value && TAB != 0) {
     if (nr >= 2) {
       run_gather_solo<D, MM, 2, TAB>(sv, w, n, T, grid, rs, nr, out, ldo, s);

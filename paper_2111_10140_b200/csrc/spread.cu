@@ -89,7 +89,7 @@ static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t ld
   if (sv.tc && w.d == 3)
     return launch_spread_tc3(sv, w, p->n, p->kb_tab, alpha, lda, R, p->grids, p->grid_total, s);
   if (sv.tc) return launch_spread_tc(sv, w, p->n, p->kb_tab, alpha, lda, R, p->grids, p->grid_total, s);
-  const int rg = v2_rhs_group(w.d, p->m, R);
+  const int rg = v2_rhs_group(w.d, p->m, R, true);
   if (rg < 1) return false;
   for (int r0 = 0; r0 < R; r0 += rg) {
     const int nr = std::min(rg, R - r0);
@@ -106,7 +106,7 @@ static bool spread_v2_window(afs_plan* p, int l, const double* alpha, int64_t ld
   return true;
 }
 
-int v2_rhs_group(int D, int m, int R) {
+int v2_rhs_group(int D, int m, int R, bool spread) {
   // mirrors Fits<> in sliding.cuh: LPL * 2m * RG <= 64 doubles, RG = 2 only for m <= 4
   const int W = 2 * m;
   const int lines = D == 3 ? W * W : (D == 2 ? W : 1);
@@ -118,6 +118,10 @@ int v2_rhs_group(int D, int m, int R) {
   }
   const int lpl = (lines + team - 1) / team;
   if (lpl * W > 64) return 0;
+  // 3-D spread at m = 4 with many right-hand sides: 4 per pass (window values evaluated half
+  // as often, same 2 blocks/SM as 2 per pass; C4 at N=1e8: spread 51.5 -> 41.7 ms).  The
+  // gather's 4-RHS variant spills (255 registers) and is slower, so it keeps 2.
+  if (spread && D == 3 && R >= 4 && m == 4 && lpl * W * 4 <= 64) return 4;
   if (R >= 2 && m <= 4 && lpl * W * 2 <= 64) return 2;
   return 1;
 }
