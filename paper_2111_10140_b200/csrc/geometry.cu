@@ -255,9 +255,10 @@ __global__ void k_pad_tc(const int32_t* __restrict__ counts, const int64_t* __re
 }
 
 bool tc_eligible(int d, int m, int tab, int n, int64_t N) {
-  // 8-offset stencils (m = 4) on a compile-time table; 14-bit cells in the group header;
-  // int32 node indices in the kernels
-  if (d != 2 || m != 4 || tab == 0 || n > (1 << 14) || N >= (int64_t)INT32_MAX / 2) return false;
+  // 8-offset stencils (m = 4) on a compile-time table; int32 node indices in the kernels;
+  // the plan build scans a table of 4 n^2 half-cells on the host, so n is kept <= 2048
+  // (the header itself would allow 14-bit cells)
+  if (d != 2 || m != 4 || tab == 0 || n > 2048 || N >= (int64_t)INT32_MAX / 2) return false;
   const char* e = getenv("AFS_TC");   // A/B hook: AFS_TC=0 keeps the FMA kernels
   return !(e && e[0] == '0');
 }
