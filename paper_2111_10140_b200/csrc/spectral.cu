@@ -304,8 +304,13 @@ __device__ __forceinline__ void dft_reg(double2 (&v)[R], const double2 (&w)[R / 
   }
 }
 
+// blocks per SM (register cap): 6 for n <= 128 (no spills; C2 spectral 0.132 -> 0.114 ms),
+// 4 for n = 256 (a cap of 6 spills and is slower), 2 from n = 512
 template <int N1, int N2>
-__global__ void __launch_bounds__(128, (N1 * N2 >= 512) ? 2 : 4) k_line_pass_4s(const LinePass p, const BatchOff off,
+constexpr int line4s_min_blocks() { return N1 * N2 >= 512 ? 2 : (N1 * N2 >= 256 ? 4 : 6); }
+
+template <int N1, int N2>
+__global__ void __launch_bounds__(128, line4s_min_blocks<N1, N2>()) k_line_pass_4s(const LinePass p, const BatchOff off,
                                                       const double2* __restrict__ twg, int lpc,
                                                       int T) {
   constexpr int n = N1 * N2;
