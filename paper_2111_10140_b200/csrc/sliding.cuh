@@ -357,8 +357,15 @@ __global__ void __launch_bounds__(128, v2_min_blocks<D, MM, RG>()) k_spread_v2(c
 #pragma unroll
       for (int p = 0; p < P; ++p)
         if (live[p]) {
+          if constexpr (RG == 1 && D >= 2) {
+            // one right-hand side: fold alpha into the last dimension's staged values, so
+            // the per-node loop of every lane skips one load and one multiply per line
 #pragma unroll
-          for (int r = 0; r < RG; ++r) rows[p][S::A_OFF + r] = a[p][r];
+            for (int k = 0; k < W; ++k) rows[p][(D - 1) * W + k] *= a[p][0];
+          } else {
+#pragma unroll
+            for (int r = 0; r < RG; ++r) rows[p][S::A_OFF + r] = a[p][r];
+          }
         }
     }
     __syncwarp();
@@ -382,7 +389,8 @@ __global__ void __launch_bounds__(128, v2_min_blocks<D, MM, RG>()) k_spread_v2(c
           const double lw = line_weight<D, MM>(row, lg[j]);
 #pragma unroll
           for (int r = 0; r < RG; ++r) {
-            const double p = lw * row[S::A_OFF + r];
+            // RG == 1, D >= 2: alpha is folded into wl at staging
+            const double p = (RG == 1 && D >= 2) ? lw : lw * row[S::A_OFF + r];
 #pragma unroll
             for (int k = 0; k < W; ++k) acc[j][k][r] = fma(p, wl[k], acc[j][k][r]);
           }
