@@ -1,0 +1,39 @@
+"""Ad-hoc GPU fuzz: random operators against the oracle (python tools/fuzz_many.py)."""
+import sys, os
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+import numpy as np
+import paper_2111_10140_b200 as afs
+from oracle import fastsum_oracle as orc
+def clustered(rng, N, d, k=3, std=0.01):
+    centers = rng.uniform(-0.2, 0.2, size=(k, d))
+    X = centers[rng.integers(0, k, size=N)] + std * rng.standard_normal((N, d))
+    return np.clip(X, -0.25, np.nextafter(0.25, 0.0))
+rng = np.random.default_rng(777)
+worst = 0; fails = 0
+for k in range(120):
+    d_total = int(rng.integers(1, 6)); P = int(rng.integers(1, 5))
+    windows = []
+    for _ in range(P):
+        dw = int(rng.integers(1, min(3, d_total) + 1))
+        windows.append(tuple(sorted(rng.choice(d_total, size=dw, replace=False).tolist())))
+    M = int(rng.choice([4, 8, 16, 32, 64])); m = int(rng.choice([1, 2, 3, 4, 4, 4, 5, 6]))
+    os_ = float(rng.choice([2.0, 1.5, 1.25])); sigma = float(rng.uniform(0.02, 3.0))
+    N = int(rng.integers(1, 3000)); Nt = int(rng.choice([0, 0, 1, 500])); R = int(rng.integers(1, 7))
+    tc3 = bool(rng.integers(0, 2)); os.environ["AFS_TC3"] = "1" if tc3 else "0"
+    X = clustered(rng, N, d_total) if rng.integers(0, 2) else rng.normal(size=(N, d_total)) * 3
+    Z = rng.normal(size=(Nt, d_total)) if Nt else None
+    A = rng.standard_normal((N, R))
+    try:
+        op = afs.AnovaKernelOperator(X, windows, sigma, afs.AccuracyProfile("f", os_, m), Z,
+                                     afs.PeriodizationConfig(coeff_grid=M), strict=False, max_rhs=R)
+        got = op.apply(A if R > 1 else A[:, 0]).reshape(Nt if Nt else N, -1)
+        for r in range(R):
+            want = orc.anova_apply(X, windows, A[:, r], sigma, M, m, os_, Z)
+            nw = np.linalg.norm(want)
+            err = np.linalg.norm(got[:, r] - want) / nw if nw > 0 else np.linalg.norm(got[:, r])
+            worst = max(worst, err)
+            if not err < 1e-10:
+                fails += 1; print("FAIL", k, dict(d_total=d_total, windows=windows, M=M, m=m, os=os_, N=N, Nt=Nt, R=R, tc3=tc3), r, err); break
+    except Exception as e:
+        print("EXC", k, dict(d_total=d_total, windows=windows, M=M, m=m, os=os_, N=N, Nt=Nt, R=R), type(e).__name__, str(e)[:200])
+print("done worst", worst, "fails", fails)
