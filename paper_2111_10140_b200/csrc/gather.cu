@@ -163,6 +163,9 @@ int gather_branches(const afs_plan* p, int R) {
   return nb;
 }
 
+bool gather_1d_fusable(const afs_plan* p);
+void gather_1d_fused(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
+
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
   // out = 0, then out += eta_l * s_l in window order (anova.py:179-183)
   AFS_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * p->Nt, R, s));
@@ -184,12 +187,25 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
       for (int b = 1; b < nb; ++b)
         AFS_CUDA(cudaMemsetAsync(p->outx[b - 1], 0, sizeof(double) * p->Nt * R, p->aux[b - 1]));
     }
+    // all 1-D windows in one fused launch (gather1d.cu) at the first 1-D window's place
+    std::vector<char> fused(p->P, 0);
+    int first1d = -1;
+    if (p->window_eval == 0 && gather_1d_fusable(p))
+      for (int l = 0; l < p->P; ++l)
+        if (p->win[l].d == 1) {
+          fused[l] = 1;
+          if (first1d < 0) first1d = l;
+        }
     for (int l = 0; l < p->P; ++l) {
       if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
       const int br = l % nb;
       const cudaStream_t sl = br ? p->aux[br - 1] : s;
       double* o = br ? p->outx[br - 1] : out;
       const int64_t lo = br ? p->Nt : ldo;
+      if (fused[l]) {
+        if (l == first1d) gather_1d_fused(p, o, lo, R, sl);
+        continue;
+      }
       if (!gather_v2_window(p, l, o, lo, R, sl)) gather_v1(p, l, l + 1, o, lo, R, sl);
     }
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
