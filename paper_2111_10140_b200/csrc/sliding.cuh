@@ -572,5 +572,9 @@ bool launch_gather_v2(const SortedSide& sv, const Window& w, int n, int m, int t
                       const double* grid, int64_t rs, int nr, double* out, int64_t ldo,
                       cudaStream_t s);
 int v2_rhs_group(int D, int m, int R, bool spread);   // right-hand sides per pass
+struct SoloBatch;   // solo.cuh
+void launch_spread_solo_batch_1d(const SoloBatch& B, int n, int m, int tab, const PolyTable& T,
+                                 const double* alpha, int64_t lda, int R, double* grid, int64_t rs,
+                                 cudaStream_t s);
 
 }  // namespace afs

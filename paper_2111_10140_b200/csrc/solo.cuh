@@ -131,12 +131,50 @@ __device__ __forceinline__ int warp_max_i(int v) {
 // spread
 // ----------------------------------------------------------------------------
 template <int D, int MM, int RG, int TAB>
+__device__ __forceinline__ void spread_solo_body(const SortedSide& sv, const Window& w, int n,
+                                                 const PolyTable& T,
+                                                 const double* __restrict__ alpha,
+                                                 int64_t lda, int nr,
+                                                 double* __restrict__ grid,
+                                                 int64_t rhs_stride);
+
+template <int D, int MM, int RG, int TAB>
 __global__ void __launch_bounds__(128) k_spread_solo(const SortedSide sv, const Window w, int n,
                                                      const PolyTable T,
                                                      const double* __restrict__ alpha,
                                                      int64_t lda, int nr,
                                                      double* __restrict__ grid,
                                                      int64_t rhs_stride) {
+  spread_solo_body<D, MM, RG, TAB>(sv, w, n, T, alpha, lda, nr, grid, rhs_stride);
+}
+
+// all windows of a batch in one launch (blockIdx.y = window; their grids are disjoint), so
+// the small 1-D spreads of a plan share one launch instead of one tail each
+constexpr int kSoloBatch = 40;
+struct SoloBatch {
+  int nwin;
+  SortedSide sv[kSoloBatch];
+  Window w[kSoloBatch];
+};
+
+template <int D, int MM, int RG, int TAB>
+__global__ void __launch_bounds__(128) k_spread_solo_batch(const __grid_constant__ SoloBatch B, int n,
+                                                           const __grid_constant__ PolyTable T,
+                                                           const double* __restrict__ alpha,
+                                                           int64_t lda, int nr,
+                                                           double* __restrict__ grid,
+                                                           int64_t rhs_stride) {
+  spread_solo_body<D, MM, RG, TAB>(B.sv[blockIdx.y], B.w[blockIdx.y], n, T, alpha, lda, nr, grid,
+                                   rhs_stride);
+}
+
+template <int D, int MM, int RG, int TAB>
+__device__ __forceinline__ void spread_solo_body(const SortedSide& sv, const Window& w, int n,
+                                                 const PolyTable& T,
+                                                 const double* __restrict__ alpha,
+                                                 int64_t lda, int nr,
+                                                 double* __restrict__ grid,
+                                                 int64_t rhs_stride) {
   using C = SoloCfg<D, MM>;
   constexpr int W = C::W, LINES = C::LINES, NACC = C::NACC;
   const int lane = threadIdx.x & 31;

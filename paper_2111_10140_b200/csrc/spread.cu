@@ -10,6 +10,7 @@
 #include "sliding.cuh"
 #include "tc2d.cuh"
 #include "tc3d.cuh"
+#include "solo.cuh"
 
 namespace afs {
 
@@ -223,11 +224,36 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   // branches (not while timing windows): window l runs on branch l % nb
   const int nb = timed ? 1 : spread_branches(p);
   if (nb > 1) fork_branches(p, nb, s);
+  // the 1-D windows' solo spreads share one launch (grids disjoint), at the first 1-D
+  // window's place; AFS_SPREAD1D=0 keeps one launch per window
+  std::vector<int> ones;
+  if (p->window_eval == 0 && p->P > 1) {
+    const char* e = getenv("AFS_SPREAD1D");
+    if (!(e && e[0] == '0'))
+      for (int l = 0; l < p->P; ++l)
+        if (p->win[l].d == 1 && !p->src_side[l]->tc) ones.push_back(l);
+    if (ones.size() < 2) ones.clear();
+  }
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[l], s));
     const int br = l % nb;
     const cudaStream_t sl = br ? p->aux[br - 1] : s;
+    if (!ones.empty() && w.d == 1) {
+      if (l == ones[0]) {
+        for (size_t b0 = 0; b0 < ones.size(); b0 += kSoloBatch) {
+          SoloBatch B{};
+          B.nwin = (int)std::min<size_t>(kSoloBatch, ones.size() - b0);
+          for (int i = 0; i < B.nwin; ++i) {
+            B.sv[i] = *p->src_side[ones[b0 + i]];
+            B.w[i] = p->win[ones[b0 + i]];
+          }
+          launch_spread_solo_batch_1d(B, p->n, p->m, p->kb_tab, *p->poly, alpha, lda, R, p->grids,
+                                      p->grid_total, sl);
+        }
+      }
+      continue;
+    }
     if (spread_v2_window(p, l, alpha, lda, R, sl)) continue;
     switch (p->m) {
       case 1: launch_spread_m<1>(p, w, alpha, lda, R, sl); break;
