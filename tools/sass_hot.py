@@ -4,7 +4,7 @@ import csv
 import collections
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
+rows = list(csv.reader(open(sys.argv[1], encoding='utf-8', errors='replace')))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 kernels = []
 cur = None
