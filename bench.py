@@ -81,7 +81,8 @@ def algorithmic_bytes(N, windows, n, R=1):
 
 
 def lpt_assign(windows, N, m, world):
-    """Longest-processing-time deal of windows to ranks on cost N*(2m)^d."""
+    """Longest-processing-time deal of windows to ranks on the modelled kernel time
+    (distributed.window_costs)."""
     from paper_2111_10140_b200.distributed import lpt_assign as lpt, window_costs
 
     return lpt(window_costs(windows, N, m), world)

@@ -41,8 +41,20 @@ def lpt_assign(costs, world):
 
 
 def window_costs(windows, N, m):
-    """Spread+gather touch cost of each window, N (2m)^d_l."""
-    return [float(N) * (2 * m) ** len(w) for w in windows]
+    """Modelled spread+gather time of each window: N x fp64 work per node / pipe efficiency.
+
+    Work per node and pass = touches (2m)^d + window values 2m d 12 (12-term polynomials)
+    + line products (2m)^(d-1); efficiency 0.74 for the tensor-core 2-D kernels (m = 4),
+    0.58 for the FMA kernels (profiles/r01_ncu_final.txt).  At m = 4 this prices a 3-D
+    window at 4.2 2-D windows, as measured on C3 (1.86 vs 0.47 ms); the bare touch count
+    (N (2m)^d) would say 8 and leave the 8-rank deal of C3 at 83% balance."""
+    costs = []
+    for w in windows:
+        d = len(w)
+        work = (2 * m) ** d + 2 * m * d * 12 + (2 * m) ** (d - 1)
+        eff = 0.74 if (d == 2 and m == 4) else 0.58
+        costs.append(float(N) * work / eff)
+    return costs
 
 
 class WindowSharded:
