@@ -388,9 +388,12 @@ def run_ours(args):
         for i in range(max(1, args.e2e_steps) + warm):
             barrier()
             t0 = time.perf_counter()
-            res = op.apply(x)                          # H2D alpha, matvec, D2H partial
-            if dist is not None:
-                part = (res if torch.is_tensor(res) else torch.from_numpy(res)).to(dev)
+            if dist is None:
+                res = op.apply(x)                      # H2D alpha, matvec, D2H result
+            else:
+                # H2D alpha, this rank's windows on the device, all-reduce, D2H of the sum
+                xt = x if torch.is_tensor(x) else torch.from_numpy(x)
+                part = op.apply(xt.to(dev, non_blocking=True))
                 dist.all_reduce(part)
                 res = part.cpu()
             torch.cuda.synchronize()
