@@ -478,7 +478,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * w.N,
                     "d2h_bytes_per_step": 8 * w.N,
-                    "path": "AnovaKernelOperator.apply(pinned torch CPU alpha) -> pinned CPU result",
+                    "path": ("AnovaKernelOperator.apply(pinned torch CPU alpha) -> pinned CPU result"
+                             if world == 1 else
+                             "pinned alpha -> device; AnovaKernelOperator.apply on this rank's windows; "
+                             "NCCL all-reduce; D2H of the sum"),
                     "pageable_numpy_value": 1.0 / e2e_pageable_s},
             "clocks": clk.summary(),
             "gpu_launches": info["kernel_launches_per_apply"] * args.steps,
