@@ -471,8 +471,9 @@ def run_ours(args):
                                   "frac": fp64_tflops / fp64_peak, "peak_source": fp64_src,
                                   "fma_per_node": fma_per_node},
                          "note": "m=4 makes the kernel fp64-pipe-bound (DESIGN.md §5); 2-D windows at "
-                                 "m=4 run on the fp64 tensor cores (DMMA, 256 MACs/node executed vs "
-                                 "the 248 algorithmic FMAs counted here); traffic = ncu dram "
+                                 "m=4 run on the fp64 tensor cores (DMMA: the spread executes 256 "
+                                 "MACs/node, the gather 192 plus 1024 per half-cell, vs the 248 "
+                                 "algorithmic FMAs counted here); traffic = ncu dram "
                                  "read+write per launch (profiles/)"},
             "window_ms": {"spread": win_sp, "gather": win_ga},
             "cpu_baseline": cpu,

@@ -14,15 +14,21 @@
 //     spread  G[o][p] += sum_node alpha_node Phi_x[node][o] Phi_y[node][p] (nfft.py:241-245)
 // The fragment layouts line up without shuffles: the eval result D[row][2q+t] is directly
 // the A (gather) or, evaluated transposed, the A/B (spread) operand of the touch MMA with
-// k relabelled as offset (or node) 2k+t.  Per group: 8 DMMAs = 2048 fp64 MACs, against
-// ~1980 DFMAs of the lane-private FMA kernels (solo.cuh) -- the same arithmetic, but one
-// instruction per 256 MACs, so the fp64 pipe stops waiting on issue.
+// k relabelled as offset (or node) 2k+t.  Per group the spread runs 8 DMMAs = 2048 fp64
+// MACs, against ~1980 DFMAs of the lane-private FMA kernels (solo.cuh) -- the same
+// arithmetic, but one instruction per 256 MACs, so the fp64 pipe stops waiting on issue.
+// The gather folds Phi_x's coefficient matrix into the grid once per half-cell
+// (P_x (C G) instead of (P_x C) G, see k_gather_tc) and runs 6 per group.
 #pragma once
 
 #include <algorithm>
 
-#ifndef AFS_TC_MINB
-#define AFS_TC_MINB 1   // __launch_bounds__ min blocks per SM (register cap), tuning hook
+// __launch_bounds__ min blocks per SM (register caps) of the one-rhs gather and spread, tuning hooks
+#ifndef AFS_TC_MINB_GATHER
+#define AFS_TC_MINB_GATHER 5
+#endif
+#ifndef AFS_TC_MINB_SPREAD
+#define AFS_TC_MINB_SPREAD 1
 #endif
 
 #include "geometry.cuh"
@@ -156,16 +162,66 @@ __device__ __forceinline__ void tc_stage_vals(TcRing<U, D, RG>& R, int st, const
 }
 
 // ----------------------------------------------------------------------------
-// gather: out[perm] += eta * interp over groups [g0, g1) of one warp, U at a time
+// gather: out[perm] += eta * interp over groups [g0, g1) of one warp, U at a time.
+//
+// The x-dimension window matrix is folded into the grid once per half-cell:
+//     s_node = sum_p (P_x Ghat)[node][p] Phi_y[node][p],   Ghat[k][p] = sum_o C[o][k] G[o][p]
+// (P_x the node powers, C the polynomial table), so a group costs 3 DMMAs for P_x Ghat and 3 for
+// Phi_y instead of 3 + 3 + 2, and Ghat (4 DMMAs, computed as Ghat^T = G^T C so its accumulator
+// is directly the B operand) is paid once per header change (~19 groups at C3).  Ghat^T's
+// fragment gives lane (p, q) the terms k = 2q + {0, 1} and, of the upper block, 8 + 2q + {0, 1}
+// for q < 2: one xor-2 shuffle hands lanes q >= 2 the odd ones, so the third k-step runs over
+// k = 8 + 2 (q & 1) + (q >> 1) and the node powers follow that order (tc_powers_ghat).
 // ----------------------------------------------------------------------------
+// lane's Ghat coefficient fragment: B[kk = q][n = slot] = C[o = 2q + t][k = slot + 8b]
+template <int TAB>
+__device__ __forceinline__ void tc_coefs_ghat(int lane, double (&cg)[2][2]) {
+  constexpr int NT = TcPoly<TAB>::NT;
+  static_assert(NT > 8 && NT <= 12, "three k-steps of the folded gather");
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int k = (lane >> 2) + 8 * b, o = 2 * (lane & 3) + t;
+      const double c = k < NT ? kb_coef<TAB, 4>(o, k) : 0.0;
+      asm volatile("mov.b64 %0, %1;" : "=d"(cg[b][t]) : "d"(c));
+    }
+}
+
+// powers in the folded gather's k order: x^(2q), x^(2q+1), x^(8 + 2 (q & 1) + (q >> 1))
+__device__ __forceinline__ void tc_powers_ghat(double x, bool q1, bool q2, double (&pw)[3]) {
+  const double x2 = x * x;
+  const double x4 = x2 * x2;
+  const double x8 = x4 * x4;
+  const double s1 = q1 ? x2 : 1.0;
+  pw[0] = s1 * (q2 ? x4 : 1.0);
+  pw[1] = pw[0] * x;
+  pw[2] = x8 * s1 * (q2 ? x : 1.0);
+}
+
+// Ghat fragments of one half-cell from the lane's grid values ga = G[2q][slot], gc = G[2q+1][slot]
+__device__ __forceinline__ void tc_ghat(double ga, double gc, const double (&cg)[2][2], bool q2,
+                                        double (&gh)[3]) {
+  double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+  dmma884(d0, ga, cg[0][0]);
+  dmma884(d0, gc, cg[0][1]);
+  dmma884(d1, ga, cg[1][0]);
+  dmma884(d1, gc, cg[1][1]);
+  const double odd = __shfl_xor_sync(0xffffffffu, d1[1], 2);
+  gh[0] = d0[0];
+  gh[1] = d0[1];
+  gh[2] = q2 ? odd : d1[0];
+}
+
 template <int RG, int TAB, int U, bool POW2, int D>
-__global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_GATHER : 1) k_gather_tc(const SortedSide sv, const Window w, int n,
                                                    const double* __restrict__ grid,
                                                    int64_t rhs_stride, int nr,
                                                    double* __restrict__ out, int64_t ldo,
                                                    int gpw) {
   static_assert(D >= 4, "values are staged two batches ahead of node data landing");
   constexpr int NKS = TcPoly<TAB>::NKS;
+  static_assert(NKS == 3, "three k-steps per window matrix");
   __shared__ TcRing<U, D, RG> ring[4];
   const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
   const bool q1 = q & 1, q2 = q >= 2;
@@ -176,18 +232,20 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
   // gpw is a multiple of U and the layout carries >= D*U trailing empty groups, so the last
   // warp may run (and prefetch) past ngroups without clamping
   const int g1 = min(g0 + gpw, (int)sv.ngroups);
-  double cf[NKS];
+  double cf[NKS], cg[2][2];
   tc_coefs<TAB>(lane, cf);
+  tc_coefs_ghat<TAB>(lane, cg);
   const double* g = grid + w.grid_off;
 
-  // grid operands of one batch: B[k][p] = G[cell(o = 2k + t)][cell(p)], k = lane%4,
-  // p = lane/4; reloaded only when the group header changes (a half-cell spans ~N/(4 n^2)
-  // nodes, 19 groups on average at C3)
+  // raw grid operands of one batch, ga = G[cell(o = 2q)][cell(p = slot)], gc = o = 2q + 1,
+  // loaded one batch ahead for the groups whose header differs from the previous group's
+  // (bit u of chg; a half-cell spans ~N/(4 n^2) nodes, 19 groups on average at C3)
   struct Win {
     double ga[U][RG], gc[U][RG];
   };
   int32_t hlast = -1;
-  auto load_win = [&](int st, Win& d, const Win& prev) {
+  auto load_win = [&](int st, Win& d, unsigned& chg) {
+    chg = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t h = R.hdr[st][u];
@@ -202,12 +260,7 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
           d.gc[u][r] = __ldg(gr + rb);
         }
         hlast = h;
-      } else {
-#pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          d.ga[u][r] = u == 0 ? prev.ga[U - 1][r] : d.ga[u - 1][r];
-          d.gc[u][r] = u == 0 ? prev.gc[U - 1][r] : d.gc[u - 1][r];
-        }
+        chg |= 1u << u;
       }
     }
   };
@@ -225,7 +278,9 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
   cp_async_wait<0>();
   __syncwarp();
   Win wnext;
-  load_win(0, wnext, wnext);   // hlast = -1: every group loads
+  unsigned chg_next;
+  load_win(0, wnext, chg_next);   // hlast = -1: the first group loads
+  double ghp[RG][3] = {};         // Ghat of the previous group
   int st = 0;
 #pragma unroll 1
   for (int gb = g0; gb < g1; gb += U) {
@@ -244,43 +299,43 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
 #pragma unroll
     for (int r = 0; r < RG; ++r) prior[r] = R.val[st][r][ug * 8 + slot];
     const Win wcur = wnext;
+    const unsigned chg = chg_next;
     const int st1 = st + 1 == D ? 0 : st + 1;
     const int st2 = st1 + 1 == D ? 0 : st1 + 1;
     __syncwarp();
     tc_stage_nodes(R, st, sv, gb + D * U, lane);   // refill the slot just read
     tc_stage_vals(R, st2, out, ldo, nr, lane);       // values of batch b + 2
     cp_async_commit();
-    load_win(st1, wnext, wcur);                      // grid window of batch b + 1
-    // window values Phi[node][o], o = 2q, 2q+1
-    double fx[U][2], fy[U][2];
+    load_win(st1, wnext, chg_next);                  // grid window of batch b + 1
+    // per group: Ghat (recomputed where the header changed), the y window values
+    // Phi_y[node][o], o = 2q, 2q+1, and the lane partials P_x Ghat . Phi_y
+    double sp[RG][U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      double px[NKS], py[NKS];
-      tc_powers<NKS>(x0[u], q1, q2, px);
-      tc_powers<NKS>(x1[u], q1, q2, py);
-      fx[u][0] = fx[u][1] = fy[u][0] = fy[u][1] = 0.0;
+      if (chg & (1u << u))   // warp-uniform
 #pragma unroll
-      for (int s = 0; s < NKS; ++s) {
-        dmma884(fx[u], px[s], cf[s]);
-        dmma884(fy[u], py[s], cf[s]);
+        for (int r = 0; r < RG; ++r) tc_ghat(wcur.ga[u][r], wcur.gc[u][r], cg, q2, ghp[r]);
+      double py[NKS], px[3], fy[2] = {0.0, 0.0};
+      tc_powers<NKS>(x1[u], q1, q2, py);
+      tc_powers_ghat(x0[u], q1, q2, px);
+#pragma unroll
+      for (int s = 0; s < NKS; ++s) dmma884(fy, py[s], cf[s]);
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        double t[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 3; ++s) dmma884(t, px[s], ghp[r][s]);
+        sp[r][u] = fma(t[1], fy[1], t[0] * fy[0]);
       }
     }
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
-      // lane partials of the 4 groups, then a transposed reduction over the quad: 3 shuffles
-      // instead of 8, and every lane finishes one node
-      double sp[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double t[2] = {0.0, 0.0};
-        dmma884(t, fx[u][0], wcur.ga[u][r]);
-        dmma884(t, fx[u][1], wcur.gc[u][r]);
-        sp[u] = fma(t[1], fy[u][1], t[0] * fy[u][0]);
-      }
+      // transposed reduction of the 4 groups' partials over the quad: 3 shuffles instead
+      // of 8, and every lane finishes one node
       const bool b0 = q & 1, b1 = (q >> 1) & 1;
       // xor 1: keep groups {2 b0, 2 b0 + 1}
-      const double k0 = b0 ? sp[2] : sp[0], k1 = b0 ? sp[3] : sp[1];
-      const double g0 = b0 ? sp[0] : sp[2], g1 = b0 ? sp[1] : sp[3];
+      const double k0 = b0 ? sp[r][2] : sp[r][0], k1 = b0 ? sp[r][3] : sp[r][1];
+      const double g0 = b0 ? sp[r][0] : sp[r][2], g1 = b0 ? sp[r][1] : sp[r][3];
       const double v0 = k0 + __shfl_xor_sync(0xffffffffu, g0, 1);
       const double v1 = k1 + __shfl_xor_sync(0xffffffffu, g1, 1);
       // xor 2: keep group 2 b0 + b1
@@ -298,7 +353,7 @@ __global__ void __launch_bounds__(128, AFS_TC_MINB) k_gather_tc(const SortedSide
 // (RED.F64 / fixed-point limbs) when the group header changes
 // ----------------------------------------------------------------------------
 template <int RG, int TAB, int U, bool POW2, int D>
-__global__ void __launch_bounds__(128, AFS_TC_MINB) k_spread_tc(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_SPREAD : 1) k_spread_tc(const SortedSide sv, const Window w, int n,
                                                    const double* __restrict__ alpha, int64_t lda,
                                                    int nr, double* __restrict__ grid,
                                                    int64_t rhs_stride, int gpw) {
