@@ -76,6 +76,27 @@ __device__ __forceinline__ void tc_powers(double x, bool q1, bool q2, double (&p
   if constexpr (NKS > 3) pw[3] = pw[2] * x4;
 }
 
+// Squares shared by the quad (spread).  The 4 lanes of a quad hold the same node, so the x^2,
+// x^4 every lane needs are computed once per batch -- lane l for node l % 8 of group l / 8
+// (the batch's 32 nodes) -- and read back from a per-warp table: 4 DMULs per batch instead of
+// 4 per group and lane (the fp64 pipe is shared with the DMMAs).  The gather measured slower
+// with the same table (its DMMA chains, not the DMULs, set its pace).
+template <int NV>
+struct TcPow {
+  double v[NV][32];   // [value][group * 8 + node]
+};
+
+// tc_powers given x^2, x^4
+template <int NKS>
+__device__ __forceinline__ void tc_powers_x24(double x, double x2, double x4, bool q1, bool q2,
+                                              double (&pw)[NKS]) {
+  const double p0 = (q1 ? x : 1.0) * (q2 ? x2 : 1.0);
+  pw[0] = p0;
+  if constexpr (NKS > 1) pw[1] = p0 * x4;
+  if constexpr (NKS > 2) pw[2] = pw[1] * x4;
+  if constexpr (NKS > 3) pw[3] = pw[2] * x4;
+}
+
 // grid cell of stencil slot o (polynomial order) for wrapped base cell u, class c (m = 4):
 // u - 3 + (c ? 7 - o : o) mod n; 7 - o = o ^ 7.  POW2: n is a power of two (mask n - 1)
 template <bool POW2>
@@ -363,6 +384,8 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_SPREAD : 1) k_sprea
   const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
   const bool q1 = q & 1, q2 = q >= 2;
   TcRing<U, D, RG>& R = ring[threadIdx.x >> 5];
+  __shared__ TcPow<4> pwt[4];   // x^2, x^4, y^2, y^4
+  TcPow<4>& PW = pwt[threadIdx.x >> 5];
   const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int g0 = warp * gpw;
   if (g0 >= sv.ngroups) return;   // warp-uniform
@@ -428,6 +451,14 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_SPREAD : 1) k_sprea
         al[u][r][1] = a2.y;
       }
     }
+    {   // shared squares of the batch's 32 nodes (TcPow): node lane % 8 of group lane / 8
+      const double xa = R.x0[st][lane], ya = R.x1[st][lane];
+      const double xa2 = xa * xa, ya2 = ya * ya;
+      PW.v[0][lane] = xa2;
+      PW.v[1][lane] = xa2 * xa2;
+      PW.v[2][lane] = ya2;
+      PW.v[3][lane] = ya2 * ya2;
+    }
     const int st1 = st + 1 == D ? 0 : st + 1;
     const int st2 = st1 + 1 == D ? 0 : st1 + 1;
     __syncwarp();
@@ -439,8 +470,9 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_SPREAD : 1) k_sprea
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       double px[NKS], py[NKS];
-      tc_powers<NKS>(x0[u], q1, q2, px);
-      tc_powers<NKS>(x1[u], q1, q2, py);
+      const int e = u * 8 + slot;
+      tc_powers_x24<NKS>(x0[u], PW.v[0][e], PW.v[1][e], q1, q2, px);
+      tc_powers_x24<NKS>(x1[u], PW.v[2][e], PW.v[3][e], q1, q2, py);
       fx[u][0] = fx[u][1] = fy[u][0] = fy[u][1] = 0.0;
 #pragma unroll
       for (int s = 0; s < NKS; ++s) {
