@@ -79,8 +79,8 @@ __device__ __forceinline__ void tc_powers(double x, bool q1, bool q2, double (&p
 // Squares shared by the quad (spread).  The 4 lanes of a quad hold the same node, so the x^2,
 // x^4 every lane needs are computed once per batch -- lane l for node l % 8 of group l / 8
 // (the batch's 32 nodes) -- and read back from a per-warp table: 4 DMULs per batch instead of
-// 4 per group and lane (the fp64 pipe is shared with the DMMAs).  The gather measured slower
-// with the same table (its DMMA chains, not the DMULs, set its pace).
+// 4 per group and lane (the fp64 pipe is shared with the DMMAs).  The gather measured 1.3%
+// slower with the same table.
 template <int NV>
 struct TcPow {
   double v[NV][32];   // [value][group * 8 + node]
