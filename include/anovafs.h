@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define AFS_ABI_VERSION 2
+#define AFS_ABI_VERSION 3
 
 enum afs_status {
   AFS_OK = 0,
@@ -155,10 +155,11 @@ int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset);
  * applies; arrays of n_windows). */
 int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, int32_t reset);
 
-/* Deterministic mode: the spread accumulates each grid cell in exact 120-bit fixed point
- * (three 40-bit limbs, 64-bit integer reductions) instead of fp64 atomics, with the scale
+/* Deterministic mode: the spread accumulates each grid cell in exact 108-bit fixed point
+ * (three 36-bit limbs, 64-bit integer reductions) instead of fp64 atomics, with the scale
  * chosen per apply from max|alpha| so no partial sum can overflow; the limbs are converted
- * back to fp64 once.  afs_apply / afs_cg_solve then return bit-identical results run to run
+ * back to fp64 once.  Plans with more than 2^27 source nodes are rejected
+ * (AFS_ERR_VALIDATION: limb headroom); a non-finite alpha yields NaN results.  afs_apply / afs_cg_solve then return bit-identical results run to run
  * for the same plan and inputs (the gather, spectral stage and CG reductions are already
  * fixed-order).  Costs 3x the grid memory for the limbs and ~2 extra passes per apply. */
 int afs_plan_set_deterministic(afs_plan* plan, int32_t enable);
@@ -169,6 +170,27 @@ int afs_plan_set_deterministic(afs_plan* plan, int32_t enable);
 int afs_cg_solve(afs_plan* plan, const double* b, double* x, double beta, double tol,
                  int32_t maxiter, int32_t* iterations, double* residual,
                  int32_t* converged, void* stream);
+
+/* CG vector kernels on caller-owned device vectors, for CG drivers whose matvec is not one
+ * plan -- window-sharded (replicated vectors, Ap all-reduced) and point-sharded (row-sharded
+ * vectors, scalars all-reduced) multi-GPU solves.  One iteration of cg_solve
+ * (krr.py:86-109) is  Ap = K p  ->  afs_cg_vec_ap  ->  afs_cg_vec_update  ->  host checks on
+ * ws[1..3]  ->  afs_cg_vec_direction.  ws: device doubles[AFS_CG_WORKSPACE_DOUBLES]:
+ *   ws[0] rs = r.r   ws[1] p.Ap   ws[2] rs_new   ws[3] non-finite flag (> 0: Ap had NaN/Inf)
+ * Each kernel writes the LOCAL partial over its n entries; a point-sharded driver sums ws[0]
+ * after init, ws[1..3] after ap and ws[2] after update across ranks before the next call.
+ *   afs_cg_vec_init:      x = 0, r = p = b, ws[0] = b.b, flags cleared, beta stored
+ *   afs_cg_vec_ap:        Ap += beta p (in place), ws[1] = p.Ap, ws[3] |= non-finite(Ap)
+ *   afs_cg_vec_update:    x += (ws[0]/ws[1]) p, r -= (ws[0]/ws[1]) Ap, ws[2] = r.r
+ *   afs_cg_vec_direction: p = r + (ws[2]/ws[0]) p, then ws[0] = ws[2]
+ * Reductions are fixed-order (run-to-run deterministic). */
+#define AFS_CG_WORKSPACE_DOUBLES 640
+int afs_cg_vec_init(const double* b, double* x, double* r, double* p, int64_t n, double beta,
+                    double* ws, void* stream);
+int afs_cg_vec_ap(double* ap, const double* p, int64_t n, double* ws, void* stream);
+int afs_cg_vec_update(double* x, double* r, const double* p, const double* ap, int64_t n,
+                      double* ws, void* stream);
+int afs_cg_vec_direction(double* p, const double* r, int64_t n, double* ws, void* stream);
 
 #ifdef __cplusplus
 }

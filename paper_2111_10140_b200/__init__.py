@@ -17,16 +17,17 @@ from .operators import (AnovaKernelOperator, FastsumOperator, FreeWindowSet, Win
                         anova_apply, anova_build, fastsum_apply, fastsum_build)
 from .krr import (CgResult, KernelSystem, KrrConfig, KrrModel, cg_solve, decision_values, fit,
                   load_model, model_from_dict, model_to_dict, predict, save_model)
-from .windowing import MisReport, ScalerStats, build_windows, mis_scores, zscore_apply, zscore_fit
+from .prep import MisReport, ScalerStats, build_windows, mis_scores, zscore_apply, zscore_fit
 from .nfft import NfftPlan, nfft_adjoint, nfft_forward, validate_nodes
 from .harness import bench_mvm, direct_sum, ndft_adjoint_direct, ndft_direct
+from .distributed import PointSharded, WindowSharded, sharded_cg
 
 __all__ = [
     "AccuracyProfile", "AnovaKernelOperator", "bench_mvm", "direct_sum", "ndft_adjoint_direct", "ndft_direct", "CgResult", "DeviceError", "FastsumOperator",
     "FreeWindowSet", "GaussianKernel", "GridSpec", "KernelSystem", "KrrConfig", "KrrModel",
-    "MisReport", "NfftPlan", "NumericalError", "PROFILES", "PeriodizationConfig", "ScalerStats", "ShapeError",
+    "MisReport", "NfftPlan", "NumericalError", "PROFILES", "PeriodizationConfig", "PointSharded", "ScalerStats", "ShapeError",
     "ValidationError", "WindowSet", "anova_apply", "anova_build", "build_windows", "cg_solve",
     "decision_values", "fastsum_apply", "fastsum_build", "fit", "load_model", "mis_scores",
     "model_from_dict", "model_to_dict", "nfft_adjoint", "nfft_forward", "predict", "regularize_kernel", "resolve_profile",
-    "save_model", "validate_nodes", "zscore_apply", "zscore_fit",
+    "save_model", "validate_nodes", "WindowSharded", "sharded_cg", "zscore_apply", "zscore_fit",
 ]

@@ -21,6 +21,8 @@ if os.environ.get("AFS_LIB"):
 AFS_OK, AFS_ERR_SHAPE, AFS_ERR_VALIDATION, AFS_ERR_NUMERICAL, AFS_ERR_CUDA, AFS_ERR_NOMEM = range(6)
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
+ABI_VERSION = 3
+CG_WORKSPACE_DOUBLES = 640   # AFS_CG_WORKSPACE_DOUBLES
 
 
 class WindowDesc(ctypes.Structure):
@@ -96,6 +98,16 @@ SIGNATURES = {
                                     ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]),
+    "afs_cg_vec_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
+    "afs_cg_vec_ap": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "afs_cg_vec_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_void_p]),
+    "afs_cg_vec_direction": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                            ctypes.c_void_p, ctypes.c_void_p]),
 }
 
 _lib = None
@@ -117,7 +129,7 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.afs_abi_version() != 2:
+        if lib.afs_abi_version() != ABI_VERSION:
             raise ImportError("libanovafs ABI version mismatch")
         _lib = lib
         return lib

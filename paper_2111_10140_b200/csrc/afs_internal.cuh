@@ -61,15 +61,14 @@ struct GraphEntry {
 };
 
 struct CgGraph {
-  cudaGraphExec_t exec = nullptr;
-  double* x = nullptr;   // key: the solution buffer and the shift baked into the graph
-  double beta = 0.0;
+  cudaGraphExec_t exec = nullptr;   // captured once per plan (plan-owned vectors, device beta)
 };
 
 struct CgScratch {
   double* r = nullptr;
   double* p = nullptr;
   double* ap = nullptr;
+  double* x = nullptr;         // the graph's solution vector (copied out after each solve)
   double* partial = nullptr;   // reduction partials
   double* scalars = nullptr;   // device scalars (see cg.cu)
   double* host_scalars = nullptr;  // pinned
@@ -154,6 +153,13 @@ void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, in
 void cg_solve_impl(afs_plan* p, const double* b, double* x, double beta, double tol,
                    int maxiter, int* iters, double* resid, int* conv, cudaStream_t s);
 void make_twiddles(afs_plan* p);
+// CG vector kernels on caller-owned vectors (cg.cu; afs_cg_vec_*)
+void cg_vec_init(const double* b, double* x, double* r, double* p, int64_t n, double beta,
+                 double* ws, cudaStream_t s);
+void cg_vec_ap(double* ap, const double* p, int64_t n, double* ws, cudaStream_t s);
+void cg_vec_update(double* x, double* r, const double* p, const double* ap, int64_t n,
+                   double* ws, cudaStream_t s);
+void cg_vec_direction(double* p, const double* r, int64_t n, double* ws, cudaStream_t s);
 void ensure_aux_streams(afs_plan* p);
 void fork_branches(afs_plan* p, int nb, cudaStream_t s);   // branches 1..nb-1 wait on s
 void join_branches(afs_plan* p, int nb, cudaStream_t s);   // s waits on branches 1..nb-1
@@ -165,9 +171,12 @@ int gather_branches(const afs_plan* p, int R);
 // ---------------------------------------------------------------------------
 // Default: one fp64 reduction (RED.E.ADD.F64); the summation order, hence the last bits,
 // depend on scheduling.  Deterministic mode: v * 2^S is split exactly into three signed
-// 40-bit limbs (|v 2^S| < 2^119 by the choice of S, afs_det_scale) that are added with
+// 36-bit limbs (|v 2^S| < 2^107 by the choice of S, k_det_scale) that are added with
 // 64-bit integer reductions -- associative, so the grid is bit-identical run to run.
-// Each limb stays below 2^63 for up to 2^23 flushes into one cell.
+// A limb sum stays below 2^63 for up to 2^27 flushes into one cell; a cell receives at
+// most one flush per source node, and afs_plan_set_deterministic rejects N > 2^27.
+constexpr int kDetLimbBits = 36;
+constexpr int kDetTopBit = 3 * kDetLimbBits - 1;   // 107
 __device__ __forceinline__ void grid_add(const Window& w, double* cell, double v) {
   if (w.det_limbs == nullptr) {
     atomicAdd(cell, v);
@@ -175,10 +184,10 @@ __device__ __forceinline__ void grid_add(const Window& w, double* cell, double v
   }
   const int64_t e = cell - w.det_base;
   const double x = v * __ldg(w.det_scale);
-  const double h = trunc(x * 0x1p-80);
-  const double r1 = fma(-h, 0x1p80, x);      // exact
-  const double m = trunc(r1 * 0x1p-40);
-  const double r2 = fma(-m, 0x1p40, r1);     // exact, |r2| < 2^40
+  const double h = trunc(x * 0x1p-72);
+  const double r1 = fma(-h, 0x1p72, x);      // exact
+  const double m = trunc(r1 * 0x1p-36);
+  const double r2 = fma(-m, 0x1p36, r1);     // exact, |r2| < 2^36
   const long long l0 = __double2ll_rn(r2), l1 = (long long)m, l2 = (long long)h;
   unsigned long long* L = reinterpret_cast<unsigned long long*>(w.det_limbs) + e;
   if (l0) atomicAdd(L, (unsigned long long)l0);

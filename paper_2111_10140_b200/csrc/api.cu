@@ -180,12 +180,14 @@ static void free_plan(afs_plan* p) {
   cudaFree(p->cg.r);
   cudaFree(p->cg.p);
   cudaFree(p->cg.ap);
+  cudaFree(p->cg.x);
   cudaFree(p->cg.partial);
   cudaFree(p->cg.scalars);
   for (int i = 0; i < 4; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (afs::GraphEntry& g : p->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (p->cg.graph.exec) cudaGraphExecDestroy(p->cg.graph.exec);
   for (cudaEvent_t e : p->wev_spread) cudaEventDestroy(e);
   for (cudaEvent_t e : p->wev_gather) cudaEventDestroy(e);
   if (p->istream) cudaStreamDestroy(p->istream);
@@ -520,6 +522,8 @@ static void refresh_det_windows(afs_plan* p) {
   for (afs::GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
     if (g.exec) cudaGraphExecDestroy(g.exec);
   p->graphs.clear();
+  if (p->cg.graph.exec) cudaGraphExecDestroy(p->cg.graph.exec);   // so does the CG solve graph
+  p->cg.graph = afs::CgGraph{};
 }
 
 int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
@@ -527,6 +531,9 @@ int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
     if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
+    if (enable && plan->Ns > ((int64_t)1 << 27))
+      throw afs::Error(AFS_ERR_VALIDATION,
+                       "deterministic mode supports at most 2^27 source nodes (limb headroom)");
     if (enable && !plan->det_limbs) {
       const size_t bytes = sizeof(long long) * 3 * (size_t)plan->grid_total * plan->max_rhs;
       AFS_CUDA(cudaMalloc(&plan->det_limbs, bytes));
@@ -604,6 +611,40 @@ int afs_cg_solve(afs_plan* plan, const double* b, double* x, double beta, double
   if (residual) *residual = res;
   if (converged) *converged = conv;
   return st;
+}
+
+int afs_cg_vec_init(const double* b, double* x, double* r, double* p, int64_t n, double beta,
+                    double* ws, void* stream) {
+  return afs::guarded([&] {
+    if (!b || !x || !r || !p || !ws) throw afs::Error(AFS_ERR_VALIDATION, "null vector");
+    if (n < 0) throw afs::Error(AFS_ERR_SHAPE, "negative vector length");
+    afs::cg_vec_init(b, x, r, p, n, beta, ws, (cudaStream_t)stream);
+  });
+}
+
+int afs_cg_vec_ap(double* ap, const double* p, int64_t n, double* ws, void* stream) {
+  return afs::guarded([&] {
+    if (!ap || !p || !ws) throw afs::Error(AFS_ERR_VALIDATION, "null vector");
+    if (n < 0) throw afs::Error(AFS_ERR_SHAPE, "negative vector length");
+    afs::cg_vec_ap(ap, p, n, ws, (cudaStream_t)stream);
+  });
+}
+
+int afs_cg_vec_update(double* x, double* r, const double* p, const double* ap, int64_t n,
+                      double* ws, void* stream) {
+  return afs::guarded([&] {
+    if (!x || !r || !p || !ap || !ws) throw afs::Error(AFS_ERR_VALIDATION, "null vector");
+    if (n < 0) throw afs::Error(AFS_ERR_SHAPE, "negative vector length");
+    afs::cg_vec_update(x, r, p, ap, n, ws, (cudaStream_t)stream);
+  });
+}
+
+int afs_cg_vec_direction(double* p, const double* r, int64_t n, double* ws, void* stream) {
+  return afs::guarded([&] {
+    if (!p || !r || !ws) throw afs::Error(AFS_ERR_VALIDATION, "null vector");
+    if (n < 0) throw afs::Error(AFS_ERR_SHAPE, "negative vector length");
+    afs::cg_vec_direction(p, r, n, ws, (cudaStream_t)stream);
+  });
 }
 
 }  // extern "C"

@@ -57,11 +57,14 @@ __global__ void __launch_bounds__(kRedThreads) k_finish(const double* __restrict
 }
 
 // Ap <- K p + beta p  (the reference's `op.apply(v) + lam * v`), partial p.Ap,
-// non-finite flag (krr.py:93).
+// non-finite flag (krr.py:93).  beta is read from device memory so that one captured solve
+// graph serves every shift.
 __global__ void __launch_bounds__(kRedThreads) k_cg_ap(double* __restrict__ ap,
-                                                      const double* __restrict__ p, double beta,
+                                                      const double* __restrict__ p,
+                                                      const double* __restrict__ beta_d,
                                                       int64_t n, double* __restrict__ partial,
                                                       double* __restrict__ flag) {
+  const double beta = *beta_d;
   double v = 0.0;
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_dir(double* __restrict__ p,
 
 // ---- device-side loop (graph conditional node) -------------------------------------------
 // ds: [0] rs  [1] pAp  [2] rs_new  [3] non-finite flag  [4] iterations  [5] status
-//     [6] tol * ||b||  [7] maxiter  [8] rs_new / rs (direction update)
+//     [6] tol * ||b||  [7] maxiter  [8] rs_new / rs (direction update)  [9] beta
 enum : int { kCgRunning = 0, kCgConverged = 1, kCgMaxiter = 2, kCgBadAp = -1, kCgBadCurv = -2,
              kCgBadRes = -3 };
 
@@ -159,11 +162,79 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_dir_dev(double* __restrict__
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
+// ---- CG vector kernels on caller-owned vectors (afs_cg_vec_*, distributed drivers) --------
+// ws (caller-owned device doubles, AFS_CG_WORKSPACE_DOUBLES): [0] rs  [1] pAp  [2] rs_new
+// [3] non-finite flag  [9] beta  [16..16+kRedBlocks) reduction partials.  Every value
+// written is a LOCAL partial over the n entries given; a point-sharded driver all-reduces
+// ws[0] after init, ws[1..3] after ap and ws[2] after update (krr.py:86-109).
+static_assert(16 + kRedBlocks <= AFS_CG_WORKSPACE_DOUBLES, "CG workspace too small");
+
+__global__ void __launch_bounds__(kRedThreads) k_vec_init(const double* __restrict__ b,
+                                                         double* __restrict__ x,
+                                                         double* __restrict__ r,
+                                                         double* __restrict__ p, int64_t n,
+                                                         double* __restrict__ partial) {
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    p[i] = bi;
+    v += bi * bi;
+  }
+  v = block_sum(v);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+}
+
+__global__ void k_vec_clear(double* ws, double beta) {
+  if (threadIdx.x < 16) ws[threadIdx.x] = threadIdx.x == 9 ? beta : 0.0;
+}
+
+__global__ void k_vec_roll(double* ws) { ws[0] = ws[2]; }
+
+void cg_vec_init(const double* b, double* x, double* r, double* p, int64_t n, double beta,
+                 double* ws, cudaStream_t s) {
+  k_vec_clear<<<1, 32, 0, s>>>(ws, beta);
+  k_vec_init<<<kRedBlocks, kRedThreads, 0, s>>>(b, x, r, p, n, ws + 16);
+  k_finish<<<1, kRedThreads, 0, s>>>(ws + 16, kRedBlocks, ws);
+  AFS_CUDA(cudaGetLastError());
+}
+
+void cg_vec_ap(double* ap, const double* p, int64_t n, double* ws, cudaStream_t s) {
+  k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(ap, p, ws + 9, n, ws + 16, ws + 3);
+  k_finish<<<1, kRedThreads, 0, s>>>(ws + 16, kRedBlocks, ws + 1);
+  AFS_CUDA(cudaGetLastError());
+}
+
+void cg_vec_update(double* x, double* r, const double* p, const double* ap, int64_t n,
+                   double* ws, cudaStream_t s) {
+  k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, ws, n, ws + 16);
+  k_finish<<<1, kRedThreads, 0, s>>>(ws + 16, kRedBlocks, ws + 2);
+  AFS_CUDA(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_vec_dir(double* __restrict__ p,
+                                                        const double* __restrict__ r,
+                                                        const double* __restrict__ ws, int64_t n) {
+  const double beta = ws[2] / ws[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+}
+
+void cg_vec_direction(double* p, const double* r, int64_t n, double* ws, cudaStream_t s) {
+  k_vec_dir<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, ws, n);
+  k_vec_roll<<<1, 1, 0, s>>>(ws);
+  AFS_CUDA(cudaGetLastError());
+}
+
 static void ensure_cg(afs_plan* pl) {
   CgScratch& c = pl->cg;
   if (c.n == pl->Ns) return;
   if (c.r) {
-    cudaFree(c.r); cudaFree(c.p); cudaFree(c.ap); cudaFree(c.partial); cudaFree(c.scalars);
+    cudaFree(c.r); cudaFree(c.p); cudaFree(c.ap); cudaFree(c.x); cudaFree(c.partial);
+    cudaFree(c.scalars);
     cudaFreeHost(c.host_scalars);
     if (c.graph.exec) cudaGraphExecDestroy(c.graph.exec);
     c.graph = CgGraph{};
@@ -172,23 +243,23 @@ static void ensure_cg(afs_plan* pl) {
   AFS_CUDA(cudaMalloc(&c.r, bytes));
   AFS_CUDA(cudaMalloc(&c.p, bytes));
   AFS_CUDA(cudaMalloc(&c.ap, bytes));
+  AFS_CUDA(cudaMalloc(&c.x, bytes));
   AFS_CUDA(cudaMalloc(&c.partial, sizeof(double) * kRedBlocks));
   AFS_CUDA(cudaMalloc(&c.scalars, sizeof(double) * 16));
   AFS_CUDA(cudaMallocHost(&c.host_scalars, sizeof(double) * 16));
   c.n = pl->Ns;
-  pl->device_bytes += 3 * bytes + sizeof(double) * (kRedBlocks + 8);
+  pl->device_bytes += 4 * bytes + sizeof(double) * (kRedBlocks + 16);
 }
 
-// Builds (or reuses) the whole-loop graph for solution buffer x and shift beta.  Returns
-// false when conditional graph nodes are unavailable (then the host loop runs).
-static bool cg_graph(afs_plan* pl, const double* b, double* x, double beta, cudaStream_t s) {
+// Builds (once per plan) the whole-loop graph.  It works on plan-owned vectors only (x, r,
+// p, Ap) with beta and the limits in device scalars, so every solve on the plan replays the
+// same graph; refresh_det_windows (api.cu) drops it when the captured stage parameters
+// change.  Returns false when conditional graph nodes are unavailable (host loop runs).
+static bool cg_graph(afs_plan* pl, const double* b, cudaStream_t s) {
   CgScratch& c = pl->cg;
-  if (c.graph.exec && c.graph.x == x && c.graph.beta == beta) return true;
-  if (c.graph.exec) {
-    cudaGraphExecDestroy(c.graph.exec);
-    c.graph = CgGraph{};
-  }
+  if (c.graph.exec) return true;
   const int64_t n = pl->Ns;
+  double* x = c.x;
   double* ds = c.scalars;
   // warm-up: one eager matvec performs the stages' first-use allocations and kernel
   // attributes, which must not happen inside the capture (overwrites Ap only)
@@ -215,7 +286,7 @@ static bool cg_graph(afs_plan* pl, const double* b, double* x, double beta, cuda
   AFS_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
     apply_stages(pl, c.p, n, c.ap, n, 1, s);
-    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, beta, n, c.partial, ds + 3);
+    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, ds + 9, n, c.partial, ds + 3);
     k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 1);
     k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.ap, ds, n, c.partial);
     k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 2);
@@ -232,8 +303,6 @@ static bool cg_graph(afs_plan* pl, const double* b, double* x, double beta, cuda
   cudaGraphDestroy(g);
   AFS_CUDA(e);
   c.graph.exec = exec;
-  c.graph.x = x;
-  c.graph.beta = beta;
   return true;
 }
 
@@ -250,10 +319,14 @@ static void cg_solve_graph(afs_plan* pl, const double* b, double* x, double beta
   hs[5] = 0.0;
   hs[6] = tol * bnorm;
   hs[7] = (double)maxiter;
-  AFS_CUDA(cudaMemcpyAsync(ds + 3, hs + 3, 5 * sizeof(double), cudaMemcpyHostToDevice, s));
+  hs[8] = 0.0;
+  hs[9] = beta;
+  AFS_CUDA(cudaMemcpyAsync(ds + 3, hs + 3, 7 * sizeof(double), cudaMemcpyHostToDevice, s));
+  AFS_CUDA(cudaMemsetAsync(c.x, 0, sizeof(double) * n, s));
   AFS_CUDA(cudaMemcpyAsync(c.r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   AFS_CUDA(cudaMemcpyAsync(c.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   AFS_CUDA(cudaGraphLaunch(c.graph.exec, s));
+  AFS_CUDA(cudaMemcpyAsync(x, c.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   AFS_CUDA(cudaMemcpyAsync(hs, ds, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   AFS_CUDA(cudaStreamSynchronize(s));
   const int it = (int)hs[4];
@@ -305,7 +378,7 @@ void cg_solve_impl(afs_plan* pl, const double* b, double* x, double beta, double
       }
       AFS_CUDA(cudaEventRecord(pl->ev_in, s));
       AFS_CUDA(cudaStreamWaitEvent(pl->istream, pl->ev_in, 0));
-      if (cg_graph(pl, b, x, beta, pl->istream)) {
+      if (cg_graph(pl, b, pl->istream)) {
         cg_solve_graph(pl, b, x, beta, tol, maxiter, iters, resid, conv, pl->istream, bnorm);
         return;   // synchronised with the host; nothing left on either stream
       }
@@ -313,10 +386,12 @@ void cg_solve_impl(afs_plan* pl, const double* b, double* x, double beta, double
   }
   AFS_CUDA(cudaMemcpyAsync(c.r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   AFS_CUDA(cudaMemcpyAsync(c.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  hs[9] = beta;
+  AFS_CUDA(cudaMemcpyAsync(ds + 9, hs + 9, sizeof(double), cudaMemcpyHostToDevice, s));
   double rs = hs[0];
   for (int it = 1; it <= maxiter; ++it) {
     apply_impl(pl, c.p, n, c.ap, n, 1, s);
-    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, beta, n, c.partial, ds + 3);
+    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, ds + 9, n, c.partial, ds + 3);
     k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 1);
     k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.ap, rs, ds + 1, n, c.partial);
     k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 2);

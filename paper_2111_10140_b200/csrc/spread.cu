@@ -135,23 +135,35 @@ __global__ void k_det_absmax(const double* __restrict__ alpha, int64_t lda, int6
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / N, j = i - r * N;
-    m = fmax(m, fabs(alpha[r * lda + j]));
+    const double a = fabs(alpha[r * lda + j]);
+    m = isfinite(a) ? fmax(m, a) : __longlong_as_double(0x7ff8000000000000LL);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  // non-negative doubles order like their bit patterns
-  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  for (int o = 16; o > 0; o >>= 1) {
+    const double q = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (isnan(m) || isnan(q)) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(m, q);
+  }
+  // non-negative doubles order like their bit patterns (the NaN marker above all finite ones)
+  if ((threadIdx.x & 31) == 0 && !(m == 0.0))
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-// S such that N * max|alpha| * max(window product) * 2^S < 2^119: every partial sum of a
-// cell fits the 120-bit limb range (log2_bound = log2(N * max product) + margin)
+// S such that N * max|alpha| * max(window product) * 2^S < 2^107: every partial sum of a
+// cell fits the 108-bit limb range (log2_bound = log2(N * max product) + margin).  A
+// non-finite alpha (NaN marker from k_det_absmax) makes every grid value NaN, as the
+// fp64-atomic spread would propagate it.
 __global__ void k_det_scale(double* aux, double log2_bound) {
   const double A = __longlong_as_double(*reinterpret_cast<const long long*>(aux));
+  if (isnan(A)) {
+    aux[1] = 0.0;
+    aux[2] = __longlong_as_double(0x7ff8000000000000LL);
+    return;
+  }
   int S = 0;
   if (A > 0.0) {
     int ea = 0;
     frexp(A, &ea);                      // A < 2^ea
-    S = 119 - (int)ceil(log2_bound) - ea;
+    S = kDetTopBit - (int)ceil(log2_bound) - ea;
   }
   S = max(-1000, min(1000, S));
   aux[1] = ldexp(1.0, S);
@@ -163,8 +175,8 @@ __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stri
                                const double* __restrict__ aux, double* __restrict__ grids) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const __int128 v = ((__int128)limbs[2 * stride + i] << 80) + ((__int128)limbs[stride + i] << 40) +
-                     (__int128)limbs[i];
+  const __int128 v = ((__int128)limbs[2 * stride + i] << (2 * kDetLimbBits)) +
+                     ((__int128)limbs[stride + i] << kDetLimbBits) + (__int128)limbs[i];
   const bool neg = v < 0;
   const unsigned __int128 u = (unsigned __int128)(neg ? -v : v);
   const double mag = __ull2double_rn((unsigned long long)(u >> 64)) * 0x1p64 +

@@ -19,6 +19,14 @@ in one exchange step per matvec:
 Both classes take the local compute as injectable backends so the
 orchestration is testable on CPU (gloo) without a GPU (tests/test_distributed.py);
 the default backends are the CUDA operators of this package.
+
+``sharded_cg`` runs the reference's CG (krr.py:76-110) over either operator
+(SURVEY §8(e)): window-sharded with replicated vectors (the matvec already
+all-reduces Ap, so every rank runs identical vector updates), point-sharded
+with row-sharded vectors and scalar all-reduces (b.b once, then per iteration
+p.Ap with the non-finite flag, and r.r).  The control loop is ``cg.run_cg``;
+the vector updates run as the fused device kernels of the C ABI
+(``afs_cg_vec_*``), or their torch CPU mirror in the gloo tests.
 """
 
 from __future__ import annotations
@@ -60,9 +68,10 @@ def window_costs(windows, N, m):
 class WindowSharded:
     """Window-sharded ANOVA operator.
 
-    ``make_local(windows, weights)`` returns a callable ``alpha -> partial`` for
-    this rank's windows (default: a CUDA ``AnovaKernelOperator`` on device
-    tensors).  ``apply`` returns the full sum on every rank.
+    ``make_local(windows, weights)`` returns, for this rank's windows, an object with
+    ``apply(alpha) -> partial`` or such a callable (default: a CUDA
+    ``AnovaKernelOperator``, kept as ``self.local``).  ``apply`` returns the full sum on
+    every rank.
     """
 
     def __init__(self, X, windows, sigma, *, M=64, m=4, oversampling=2.0, group=None,
@@ -87,22 +96,28 @@ class WindowSharded:
         import torch
 
         if self.local is not None:
-            part = self.local(alpha)
+            part = getattr(self.local, "apply", self.local)(alpha)
         else:
             part = torch.zeros_like(alpha)
         part = part.contiguous()
         self.dist.all_reduce(part, group=self.group)
         return part
 
+    @property
+    def n_sources(self):
+        return self.N
+
+    n_targets = n_sources
+    rows_sharded = False
+
 
 def _cuda_window_backend(X, sigma, M, m, oversampling, device):
     from .operators import AnovaKernelOperator
 
     def make(windows, weights):
-        op = AnovaKernelOperator(X, windows, sigma, AccuracyProfile("sharded", oversampling, m), None,
-                                 PeriodizationConfig(coeff_grid=M), strict=False, weights=weights,
-                                 device=device)
-        return op.apply
+        return AnovaKernelOperator(X, windows, sigma, AccuracyProfile("sharded", oversampling, m),
+                                   None, PeriodizationConfig(coeff_grid=M), strict=False,
+                                   weights=weights, device=device)
     return make
 
 
@@ -146,7 +161,12 @@ class PointSharded:
         grids = self.backend.spread(alpha_local)
         self.dist.all_reduce(grids, group=self.group)
         self.backend.spectral(grids)
-        return self.backend.gather(grids)
+        out = self.backend.gather(grids)
+        if alpha_local.dim() == 1 and out.dim() == 2:
+            out = out[0]
+        return out
+
+    rows_sharded = True
 
 
 class CudaPointBackend:
@@ -208,3 +228,25 @@ class CudaPointBackend:
         out = torch.empty((self.R, self.plan.Nt), dtype=torch.float64, device=self.plan.device)
         self.plan.gather_device(out, self.R)
         return out
+
+
+# --------------------------------------------------------------------------- sharded CG
+def sharded_cg(operator, b, beta, tol=1e-3, maxiter=1000, *, vectors=None, group=None):
+    """CG for (K + beta I) x = b over a sharded operator (krr.py:76-110).
+
+    ``operator.apply(p) -> K p``: a ``WindowSharded`` returns the full, all-reduced
+    vector and the CG vectors are replicated; a ``PointSharded`` returns this rank's rows,
+    the vectors are row-sharded and the three scalars are all-reduced.  ``b`` is the full
+    vector or this rank's rows accordingly.  Every rank takes the same decisions.
+    Returns a ``CgResult`` whose x is shaped like b."""
+    import torch.distributed as dist
+
+    from .cg import CudaCgVectors, run_cg
+
+    reduce = None
+    if getattr(operator, "rows_sharded", False):
+        def reduce(ws, lo, hi):
+            dist.all_reduce(ws[lo:hi], group=group)
+    if vectors is None:
+        vectors = CudaCgVectors(b.device)
+    return run_cg(operator.apply, b, beta, tol, maxiter, vectors, reduce)

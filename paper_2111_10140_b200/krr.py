@@ -1,39 +1,56 @@
-"""Conjugate-gradient kernel ridge regression on the GPU operator (krr.py:68-110).
+"""Kernel ridge regression around the GPU operator: the CG entry point and the fit /
+decision / predict / model-document wrappers (reference krr.py:68-202, 269-330).
 
-``cg_solve(apply_A, b, tol, maxiter)`` keeps the reference signature.  When
-``apply_A`` is a ``KernelSystem`` (``op + beta*I`` on an ``AnovaKernelOperator``),
-the whole loop runs device-resident through ``afs_cg_solve`` (fused vector
-updates, deterministic reductions, one scalar read-back per iteration).  Any
-other callable gets the reference's host loop unchanged (it is the
-compatibility path for user-defined operators, not the hot path).
+``cg_solve(apply_A, b, tol, maxiter)`` keeps the reference signature and routes
+by the type of ``apply_A``:
+
+* ``KernelSystem`` over an ``AnovaKernelOperator``: the whole solve is one CUDA graph
+  with a device-side loop (``afs_cg_solve``, csrc/cg.cu);
+* ``KernelSystem`` over a ``WindowSharded`` / ``PointSharded`` operator: the shared
+  control loop ``cg.run_cg`` with the fused device vector kernels and NCCL
+  all-reduces (``distributed.sharded_cg``);
+* any other callable: the same control loop on host numpy vectors (compatibility
+  path for user-defined operators, not the hot path).
+
+``fit`` builds its operator in deterministic mode (fixed-point spread, bit-identical
+run to run), so a fitted model -- and its CG iteration count -- is reproducible.
 """
 
 from __future__ import annotations
 
-import math
+import base64
+import json
 from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import NumericalError, ShapeError, ValidationError
-from .operators import AnovaKernelOperator, _torch
+from .cg import CgResult, NumpyCgVectors, run_cg
+from .errors import ShapeError, ValidationError
+from .operators import AnovaKernelOperator, WindowSet, _torch
+from .prep import ScalerStats, build_windows, mis_scores, zscore_apply, zscore_fit
+
+MODEL_FORMAT = "krr-model/1"
+RNG_NAME = "numpy-pcg64"
+DETERMINISTIC_MAX_NODES = 1 << 27   # afs_plan_set_deterministic limb headroom
+
+__all__ = ["CgResult", "KernelSystem", "KrrConfig", "KrrModel", "cg_solve", "fit",
+           "decision_values", "predict", "model_to_dict", "model_from_dict", "save_model",
+           "load_model"]
 
 
-@dataclass
-class CgResult:
-    x: np.ndarray
-    iterations: int
-    residual: float
-    converged: bool
-
-
+# ----------------------------------------------------------------------------- CG
 class KernelSystem:
-    """The SPD system matrix K + beta I of KRR training (krr.py:162-167)."""
+    """The shifted system K + beta I of KRR training (krr.py:162-167) over a GPU operator:
+    an ``AnovaKernelOperator`` or a sharded one (``distributed.WindowSharded`` /
+    ``distributed.PointSharded``).  Calling it applies the system; ``cg_solve`` solves it
+    on the device."""
 
-    def __init__(self, operator: AnovaKernelOperator, beta: float):
-        if not isinstance(operator, AnovaKernelOperator):
-            raise ValidationError("KernelSystem needs an AnovaKernelOperator")
-        if operator.n_targets != operator.n_sources:
+    def __init__(self, operator, beta: float):
+        from .distributed import PointSharded, WindowSharded
+
+        if not isinstance(operator, (AnovaKernelOperator, WindowSharded, PointSharded)):
+            raise ValidationError("KernelSystem needs an AnovaKernelOperator or a sharded operator")
+        if isinstance(operator, AnovaKernelOperator) and operator.n_targets != operator.n_sources:
             raise ValidationError("KernelSystem needs a square operator (no targets)")
         if not beta > 0:
             raise ValidationError(f"lambda must be positive, got {beta}")
@@ -43,28 +60,63 @@ class KernelSystem:
     def __call__(self, v):
         return self.operator.apply(v) + self.beta * v
 
+    def solve(self, b, tol, maxiter):
+        if isinstance(self.operator, AnovaKernelOperator):
+            return self._solve_plan(b, tol, maxiter)
+        from .distributed import sharded_cg
 
-def _device_cg(system: KernelSystem, b, tol, maxiter):
-    torch = _torch()
-    plan = system.operator._plan
-    on_dev = hasattr(b, "is_cuda") and b.is_cuda
-    bd = (b if on_dev else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)))
-    bd = bd.to(device=plan.device, dtype=torch.float64).contiguous()
-    if bd.dim() != 1 or bd.shape[0] != plan.N:
-        raise ShapeError(f"b must have length {plan.N}, got {tuple(bd.shape)}")
-    x = torch.empty_like(bd)
-    it, res, conv = plan.cg_device(bd, x, system.beta, tol, maxiter)
-    torch.cuda.current_stream(plan.device).synchronize()
-    return CgResult(x if on_dev else x.cpu().numpy(), it, res, conv)
+        torch = _torch()
+        on_device = hasattr(b, "is_cuda") and b.is_cuda
+        if not on_device:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            b = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(dev)
+        res = sharded_cg(self.operator, b, self.beta, tol, maxiter)
+        if not on_device:
+            res.x = res.x.cpu().numpy()
+        return res
+
+    def _solve_plan(self, b, tol, maxiter):
+        torch = _torch()
+        plan = self.operator._plan
+        on_device = hasattr(b, "is_cuda") and b.is_cuda
+        src = b if on_device else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64))
+        bd = src.to(device=plan.device, dtype=torch.float64).contiguous()
+        if bd.dim() != 1 or bd.shape[0] != plan.N:
+            raise ShapeError(f"b must have length {plan.N}, got {tuple(bd.shape)}")
+        x = torch.empty_like(bd)
+        it, res, conv = plan.cg_device(bd, x, self.beta, tol, maxiter)
+        torch.cuda.current_stream(plan.device).synchronize()
+        return CgResult(x if on_device else x.cpu().numpy(), it, res, conv)
 
 
-MODEL_FORMAT = "krr-model/1"
-RNG_NAME = "numpy-pcg64"
+def cg_solve(apply_A, b, tol=1e-3, maxiter=1000):
+    """CG for SPD systems from x0 = 0, no preconditioner: stops when ||r|| <= tol ||b||
+    (recurrence residual) or after maxiter iterations (reported, not fatal); NaN/Inf in
+    the recurrence raises NumericalError naming the iteration (krr.py:76-110)."""
+    if isinstance(apply_A, KernelSystem):
+        return apply_A.solve(b, tol, maxiter)
+    rhs = np.asarray(b, dtype=np.float64)
+    return run_cg(lambda v: np.asarray(apply_A(v), dtype=np.float64), rhs, 0.0, tol, maxiter,
+                  NumpyCgVectors())
+
+
+# ----------------------------------------------------------------------------- config
+# (predicate, message) pairs checked in order; messages are the reference's (API contract)
+_CONFIG_RULES = (
+    (lambda c: c.sigma > 0, lambda c: f"sigma must be positive, got {c.sigma}"),
+    (lambda c: c.lam > 0, lambda c: f"lambda must be positive, got {c.lam}"),
+    (lambda c: 0.0 < c.cg_tol < 1.0, lambda c: f"cg_tol must lie in (0, 1), got {c.cg_tol}"),
+    (lambda c: c.cg_maxiter >= 1, lambda c: "cg_maxiter must be at least 1"),
+    (lambda c: c.mis_threshold >= 0, lambda c: "mis_threshold must be nonnegative"),
+)
+# attribute -> key in the "krr-model/1" document
+_CONFIG_KEYS = {"sigma": "sigma", "lam": "lambda", "cg_tol": "cg_tol", "cg_maxiter": "cg_maxiter",
+                "profile": "profile", "mis_threshold": "mis_threshold"}
 
 
 @dataclass(frozen=True)
 class KrrConfig:
-    """KRR hyper-parameters (krr.py:25-65): sigma, lam, CG tol/maxiter, profile, MIS threshold."""
+    """KRR hyper-parameters (krr.py:25-65)."""
 
     sigma: float = 1.0
     lam: float = 1.0
@@ -74,43 +126,41 @@ class KrrConfig:
     mis_threshold: float = 0.0
 
     def __post_init__(self):
-        if self.sigma <= 0:
-            raise ValidationError(f"sigma must be positive, got {self.sigma}")
-        if self.lam <= 0:
-            raise ValidationError(f"lambda must be positive, got {self.lam}")
-        if not 0.0 < self.cg_tol < 1.0:
-            raise ValidationError(f"cg_tol must lie in (0, 1), got {self.cg_tol}")
-        if self.cg_maxiter < 1:
-            raise ValidationError("cg_maxiter must be at least 1")
-        if self.mis_threshold < 0:
-            raise ValidationError("mis_threshold must be nonnegative")
+        for ok, msg in _CONFIG_RULES:
+            if not ok(self):
+                raise ValidationError(msg(self))
 
     def to_dict(self):
-        return {"sigma": self.sigma, "lambda": self.lam, "cg_tol": self.cg_tol,
-                "cg_maxiter": self.cg_maxiter, "profile": self.profile,
-                "mis_threshold": self.mis_threshold}
+        return {key: getattr(self, attr) for attr, key in _CONFIG_KEYS.items()}
 
     @classmethod
     def from_dict(cls, d):
-        return cls(sigma=d["sigma"], lam=d["lambda"], cg_tol=d["cg_tol"],
-                   cg_maxiter=d["cg_maxiter"], profile=d["profile"],
-                   mis_threshold=d["mis_threshold"])
+        return cls(**{attr: d[key] for attr, key in _CONFIG_KEYS.items()})
 
 
+# ----------------------------------------------------------------------------- model
+@dataclass(eq=False)
 class KrrModel:
-    """Fitted KRR classifier: coefficients, windows, scaler, training nodes (krr.py:113-135)."""
+    """A fitted classifier: expansion coefficients over the scaled training rows, the
+    windows and scaler that produced them, and the CG outcome (krr.py:113-135)."""
 
-    def __init__(self, alpha, config, windows, scaler, train_scaled, column_names,
-                 cg_iterations, cg_residual, cg_converged):
-        self.alpha = np.asarray(alpha, dtype=np.float64)
-        self.config = config
-        self.windows = windows
-        self.scaler = scaler
-        self.train_scaled = np.asarray(train_scaled, dtype=np.float64)
-        self.column_names = tuple(column_names)
-        self.cg_iterations = int(cg_iterations)
-        self.cg_residual = float(cg_residual)
-        self.cg_converged = bool(cg_converged)
+    alpha: np.ndarray
+    config: KrrConfig
+    windows: WindowSet
+    scaler: ScalerStats
+    train_scaled: np.ndarray
+    column_names: tuple
+    cg_iterations: int
+    cg_residual: float
+    cg_converged: bool
+
+    def __post_init__(self):
+        self.alpha = np.asarray(self.alpha, dtype=np.float64)
+        self.train_scaled = np.asarray(self.train_scaled, dtype=np.float64)
+        self.column_names = tuple(self.column_names)
+        self.cg_iterations = int(self.cg_iterations)
+        self.cg_residual = float(self.cg_residual)
+        self.cg_converged = bool(self.cg_converged)
 
     @property
     def n_train(self):
@@ -120,82 +170,82 @@ class KrrModel:
     def n_features(self):
         return self.train_scaled.shape[1]
 
+    def operator(self, targets=None, **kw):
+        """The ANOVA operator over the training rows (targets: scaled test rows)."""
+        return AnovaKernelOperator(self.train_scaled, self.windows, self.config.sigma,
+                                   self.config.profile, targets=targets, **kw)
 
-def _training_input(X, y):
-    X = np.atleast_2d(np.asarray(X, dtype=np.float64))
-    y = np.asarray(y)
-    if X.ndim != 2 or X.shape[0] < 2:
+
+def _training_arrays(X, y):
+    """(X, y as float) after the reference's training-input checks (krr.py:137-149)."""
+    A = np.atleast_2d(np.asarray(X, dtype=np.float64))
+    lab = np.asarray(y)
+    if A.ndim != 2 or A.shape[0] < 2:
         raise ValidationError("training needs at least 2 samples")
-    if y.shape != (X.shape[0],):
+    if lab.shape != (A.shape[0],):
         raise ShapeError("labels must match the number of training rows")
-    vals = np.unique(y)
-    if not np.all(np.isin(vals, (-1, 1))):
-        raise ValidationError(f"labels must be -1 or +1, got {vals}")
-    if vals.size < 2:
+    present = np.unique(lab)
+    if not np.isin(present, (-1, 1)).all():
+        raise ValidationError(f"labels must be -1 or +1, got {present}")
+    if present.size < 2:
         raise ValidationError("training data must contain both classes")
-    return X, y.astype(np.float64)
+    return A, lab.astype(np.float64)
 
 
 def fit(X_train, y_train, config, column_names=None):
-    """z-score -> MIS ranking -> windows -> GPU ANOVA operator -> device CG (krr.py:152-178)."""
-    from .windowing import build_windows, mis_scores, zscore_apply, zscore_fit
-
-    X, y = _training_input(X_train, y_train)
-    if column_names is None:
-        column_names = tuple(f"f{i}" for i in range(X.shape[1]))
+    """z-score -> MIS windows -> GPU ANOVA operator -> device CG (krr.py:152-178)."""
+    X, y = _training_arrays(X_train, y_train)
+    names = column_names if column_names is not None else [f"f{i}" for i in range(X.shape[1])]
     scaler = zscore_fit(X)
     Xs = zscore_apply(scaler, X)
     windows = build_windows(mis_scores(Xs, y_train), config.mis_threshold)
-    op = AnovaKernelOperator(Xs, windows, config.sigma, config.profile)
-    res = cg_solve(KernelSystem(op, config.lam), y, tol=config.cg_tol, maxiter=config.cg_maxiter)
-    return KrrModel(res.x, config, windows, scaler, Xs, column_names, res.iterations,
-                    res.residual, res.converged)
+    op = AnovaKernelOperator(Xs, windows, config.sigma, config.profile,
+                             deterministic=Xs.shape[0] <= DETERMINISTIC_MAX_NODES)
+    sol = cg_solve(KernelSystem(op, config.lam), y, tol=config.cg_tol, maxiter=config.cg_maxiter)
+    op.close()
+    return KrrModel(sol.x, config, windows, scaler, Xs, names, sol.iterations, sol.residual,
+                    sol.converged)
 
 
 def decision_values(model, X_test):
-    """s(z) = sum_j alpha_j k_anova(z, x_j): operator rebuilt with targets (krr.py:181-196)."""
-    from .windowing import zscore_apply
-
-    X_test = np.atleast_2d(np.asarray(X_test, dtype=np.float64))
-    if X_test.shape[1] != model.n_features:
+    """s(z) = sum_j alpha_j k_anova(z, x_j): the operator rebuilt with the scaled test rows
+    as targets (union-bbox scaling, krr.py:181-196)."""
+    Z = np.atleast_2d(np.asarray(X_test, dtype=np.float64))
+    if Z.shape[1] != model.n_features:
         raise ValidationError(
-            f"test data has {X_test.shape[1]} columns, model was trained on {model.n_features}")
-    Zs = zscore_apply(model.scaler, X_test)
-    op = AnovaKernelOperator(model.train_scaled, model.windows, model.config.sigma,
-                             model.config.profile, targets=Zs)
-    return op.apply(model.alpha)
+            f"test data has {Z.shape[1]} columns, model was trained on {model.n_features}")
+    op = model.operator(targets=zscore_apply(model.scaler, Z))
+    out = op.apply(model.alpha)
+    op.close()
+    return out
 
 
 def predict(model, X_test):
-    """Labels in {-1, +1}; sign(0) -> +1 (krr.py:199-202)."""
+    """Labels in {-1, +1}, threshold 0 with sign(0) -> +1 (krr.py:199-202)."""
     return np.where(decision_values(model, X_test) >= 0.0, 1, -1).astype(np.int64)
 
 
-def _enc(arr):
-    import base64
-
+# ----------------------------------------------------------------------------- document
+def _b64(arr):
     return base64.b64encode(np.ascontiguousarray(arr, dtype="<f8").tobytes()).decode("ascii")
 
 
-def _dec(text, shape):
-    import base64
-
-    return np.frombuffer(base64.b64decode(text.encode("ascii")), dtype="<f8").reshape(shape).astype(
-        np.float64)
+def _unb64(text, shape):
+    raw = np.frombuffer(base64.b64decode(text.encode("ascii")), dtype="<f8")
+    return raw.reshape(shape).astype(np.float64)
 
 
 def model_to_dict(model):
-    """The reference's versioned "krr-model/1" document (krr.py:269-297)."""
+    """The versioned "krr-model/1" JSON document (krr.py:269-297)."""
     return {
         "format": MODEL_FORMAT,
         "config": model.config.to_dict(),
         "column_names": list(model.column_names),
         "windows": model.windows.to_dict(),
-        "scaler": {"means": [float(v) for v in model.scaler.means],
-                   "stds": [float(v) for v in model.scaler.stds]},
+        "scaler": {"means": model.scaler.means.tolist(), "stds": model.scaler.stds.tolist()},
         "train_shape": list(model.train_scaled.shape),
-        "alpha_b64": _enc(model.alpha),
-        "train_scaled_b64": _enc(model.train_scaled),
+        "alpha_b64": _b64(model.alpha),
+        "train_scaled_b64": _b64(model.train_scaled),
         "cg": {"iterations": model.cg_iterations, "residual": model.cg_residual,
                "converged": model.cg_converged},
         "rng": RNG_NAME,
@@ -203,70 +253,28 @@ def model_to_dict(model):
 
 
 def model_from_dict(doc):
-    from .operators import WindowSet
-    from .windowing import ScalerStats
-
     if doc.get("format") != MODEL_FORMAT:
         raise ValidationError(
             f"unsupported model format {doc.get('format')!r}, expected {MODEL_FORMAT}")
     shape = tuple(doc["train_shape"])
+    cg = doc["cg"]
     return KrrModel(
-        alpha=_dec(doc["alpha_b64"], (shape[0],)),
+        alpha=_unb64(doc["alpha_b64"], shape[:1]),
         config=KrrConfig.from_dict(doc["config"]),
-        windows=WindowSet(tuple(tuple(w) for w in doc["windows"]["windows"])),
-        scaler=ScalerStats(means=np.asarray(doc["scaler"]["means"], dtype=np.float64),
-                           stds=np.asarray(doc["scaler"]["stds"], dtype=np.float64)),
-        train_scaled=_dec(doc["train_scaled_b64"], shape),
-        column_names=tuple(doc["column_names"]),
-        cg_iterations=doc["cg"]["iterations"],
-        cg_residual=doc["cg"]["residual"],
-        cg_converged=doc["cg"]["converged"],
+        windows=WindowSet([tuple(w) for w in doc["windows"]["windows"]]),
+        scaler=ScalerStats(*(np.asarray(doc["scaler"][k], dtype=np.float64)
+                             for k in ("means", "stds"))),
+        train_scaled=_unb64(doc["train_scaled_b64"], shape),
+        column_names=doc["column_names"],
+        cg_iterations=cg["iterations"], cg_residual=cg["residual"], cg_converged=cg["converged"],
     )
 
 
 def save_model(model, path):
-    import json
-
     with open(path, "w", encoding="utf-8") as fh:
-        json.dump(model_to_dict(model), fh, indent=1)
-        fh.write("\n")
+        fh.write(json.dumps(model_to_dict(model), indent=1) + "\n")
 
 
 def load_model(path):
-    import json
-
     with open(path, encoding="utf-8") as fh:
         return model_from_dict(json.load(fh))
-
-
-def cg_solve(apply_A, b, tol=1e-3, maxiter=1000):
-    """CG for SPD systems from x0 = 0 without preconditioner; stops when
-    ||r|| <= tol ||b|| (recurrence residual) or after maxiter iterations."""
-    if isinstance(apply_A, KernelSystem):
-        return _device_cg(apply_A, b, tol, maxiter)
-    b = np.asarray(b, dtype=np.float64)
-    b_norm = float(np.linalg.norm(b))
-    x = np.zeros_like(b)
-    if b_norm == 0.0:
-        return CgResult(x, 0, 0.0, True)
-    r = b.copy()
-    p = r.copy()
-    rs = float(r @ r)
-    for it in range(1, maxiter + 1):
-        Ap = np.asarray(apply_A(p), dtype=np.float64)
-        if not np.all(np.isfinite(Ap)):
-            raise NumericalError(f"CG breakdown: non-finite operator output at iteration {it}")
-        pAp = float(p @ Ap)
-        if not math.isfinite(pAp) or pAp <= 0.0:
-            raise NumericalError(f"CG breakdown: non-positive curvature {pAp:.3e} at iteration {it}")
-        step = rs / pAp
-        x += step * p
-        r -= step * Ap
-        rs_new = float(r @ r)
-        if not math.isfinite(rs_new):
-            raise NumericalError(f"CG breakdown: non-finite residual at iteration {it}")
-        if math.sqrt(rs_new) <= tol * b_norm:
-            return CgResult(x, it, math.sqrt(rs_new) / b_norm, True)
-        p = r + (rs_new / rs) * p
-        rs = rs_new
-    return CgResult(x, maxiter, math.sqrt(rs) / b_norm, False)

@@ -101,6 +101,23 @@ def c4(N: int = 100_000_000, R: int = 8, seed: int = 4) -> Workload:
     return Workload("C4", X, alpha, [(0, 1, 2)], 0.1, 128, 4)
 
 
+def c4_shard(N_total: int = 100_000_000, R: int = 8, rank: int = 0, world: int = 1,
+             seed: int = 4) -> Workload:
+    """This rank's rows of a C4-distributed workload for the point-sharded bench: the 16
+    cluster centers come from ``seed`` (shared by all ranks, as in ``c4``); labels, noise and
+    alpha of the rank's N_total/world rows from the stream (seed, rank), so no rank draws
+    the other ranks' 1e8 x 11 values.  Same distribution as ``c4``, not the same draw."""
+    centers = np.random.default_rng(seed).uniform(-0.2, 0.2, size=(16, 3))
+    lo = N_total * rank // world
+    hi = N_total * (rank + 1) // world
+    rng = np.random.default_rng([seed, rank])
+    labels = rng.integers(0, 16, size=hi - lo)
+    X = centers[labels] + 0.02 * rng.standard_normal((hi - lo, 3))
+    np.clip(X, -0.25, np.nextafter(0.25, 0.0), out=X)
+    alpha = rng.standard_normal((hi - lo, R))
+    return Workload("C4", X, alpha, [(0, 1, 2)], 0.1, 128, 4, extra={"N_total": N_total})
+
+
 def c5(N: int = 1_000_000, seed: int = 5) -> Workload:
     """BASELINE config 4: d=20 in 5 equicorrelated blocks (rho=0.7), z-scored, 20 singles +
     10 pairs (2k,2k+1), y = sum_k f_k(x_Wk) + 0.1 eps (random-Fourier f_k), sigma=1, beta=0.1."""

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     lib.afs_abi_version.restype = ctypes.c_int
-    assert lib.afs_abi_version() == 2
+    assert lib.afs_abi_version() == 3
 
 
 def test_struct_layouts_match_header():

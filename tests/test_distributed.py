@@ -204,3 +204,104 @@ def test_point_sharded_matches_single_process(tmp_path, exchange):
     ref = orc.fastsum_apply(wl.X, wl.alpha[:, 0], wl.sigma, wl.M, wl.m)
     got = np.concatenate([np.load(out + f".{r}.npy") for r in range(2)])
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
+# --------------------------------------------------------------------------- sharded CG
+def _oracle_windows_local(w):
+    from oracle import fastsum_oracle as orc
+
+    def make_local(windows, weights):
+        def apply(alpha):
+            a = alpha.numpy()
+            s = np.zeros(w.N)
+            for eta, win in zip(weights, windows):
+                s += eta * orc.fastsum_apply(w.X[:, list(win)], a, w.sigma, w.M, w.m)
+            return torch.from_numpy(s)
+        return apply
+    return make_local
+
+
+def _cg_window_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    from paper_2111_10140_b200.cg import TorchCgVectors
+    from paper_2111_10140_b200.distributed import WindowSharded, sharded_cg
+
+    w = synthetic.c5(N=300)
+    op = WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, make_local=_oracle_windows_local(w))
+    res = sharded_cg(op, torch.from_numpy(w.y.copy()), w.beta, 1e-6, 400, vectors=TorchCgVectors())
+    np.save(out_path + f".{rank}.npy", np.concatenate([[res.iterations, res.residual],
+                                                       res.x.numpy()]))
+    dist.destroy_process_group()
+
+
+def test_window_sharded_cg_matches_single_process(tmp_path):
+    """CG with replicated vectors over window shards (one all-reduce of Ap per iteration):
+    every rank ends with the single-process solution at the same iteration count."""
+    from oracle import fastsum_oracle as orc
+
+    out = str(tmp_path / "wcg")
+    _run(_cg_window_worker, 2, out)
+    w = synthetic.c5(N=300)
+    rx, rit, _, _ = orc.cg_solve(
+        lambda v: orc.anova_apply(w.X, w.windows, v, w.sigma, w.M, w.m) + w.beta * v,
+        w.y, tol=1e-6, maxiter=400)
+    for r in range(2):
+        got = np.load(out + f".{r}.npy")
+        assert abs(int(got[0]) - rit) <= 1
+        assert np.linalg.norm(got[2:] - rx) / np.linalg.norm(rx) < 1e-8
+
+
+def _cg_point_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    from paper_2111_10140_b200.cg import TorchCgVectors
+    from paper_2111_10140_b200.distributed import PointSharded, sharded_cg
+
+    wl = synthetic.c4(N=500, R=1)
+    y = np.sin(7.0 * wl.X).sum(axis=1)
+    shard = np.array_split(np.arange(wl.N), world)[rank]
+    be = NumpyPointBackend(wl.X[shard], (0, 1, 2), wl.sigma, 16, wl.m, exchange="spectrum")
+    res = sharded_cg(PointSharded(be), torch.from_numpy(y[shard].copy()), 0.5, 1e-8, 300,
+                     vectors=TorchCgVectors())
+    np.save(out_path + f".{rank}.npy", np.concatenate([[res.iterations, res.residual],
+                                                       res.x.numpy()]))
+    dist.destroy_process_group()
+
+
+def test_point_sharded_cg_matches_single_process(tmp_path):
+    """CG with row-sharded vectors and scalar all-reduces: the stacked shards
+    equal the single-process solution, with the same iteration count and residual."""
+    from oracle import fastsum_oracle as orc
+
+    out = str(tmp_path / "pcg")
+    _run(_cg_point_worker, 2, out)
+    wl = synthetic.c4(N=500, R=1)
+    y = np.sin(7.0 * wl.X).sum(axis=1)
+    rx, rit, _, _ = orc.cg_solve(lambda v: orc.fastsum_apply(wl.X, v, wl.sigma, 16, wl.m) + 0.5 * v,
+                                 y, tol=1e-8, maxiter=300)
+    parts = [np.load(out + f".{r}.npy") for r in range(2)]
+    for p in parts:
+        assert abs(int(p[0]) - rit) <= 1
+    assert parts[0][1] == parts[1][1]           # identical decisions on every rank
+    x = np.concatenate([p[2:] for p in parts])
+    assert np.linalg.norm(x - rx) / np.linalg.norm(rx) < 1e-8
+
+
+def test_host_cg_path_is_bitwise_the_reference_loop():
+    """cg_solve on a plain callable runs the shared control loop on numpy vectors with the
+    reference's elementwise expressions (krr.py:86-109): bit-identical to the oracle loop."""
+    from oracle import fastsum_oracle as orc
+    from paper_2111_10140_b200.krr import cg_solve
+
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((60, 60))
+    A = A @ A.T + 60 * np.eye(60)
+    b = rng.standard_normal(60)
+    got = cg_solve(lambda v: A @ v, b, tol=1e-10, maxiter=200)
+    rx, rit, rres, rconv = orc.cg_solve(lambda v: A @ v, b, tol=1e-10, maxiter=200)
+    assert got.iterations == rit and got.converged == rconv
+    np.testing.assert_array_equal(got.x, rx)
+    assert got.residual == rres
+    with pytest.raises(Exception, match="non-positive curvature"):
+        cg_solve(lambda v: -v, b, tol=1e-10, maxiter=5)
+    with pytest.raises(Exception, match="non-finite operator output at iteration 1"):
+        cg_solve(lambda v: v * np.nan, b, tol=1e-10, maxiter=5)
