@@ -240,22 +240,24 @@ def ncu_traffic(key):
 # ---------------------------------------------------------------------------
 # CPU side: the UNMODIFIED reference (oracle/_ref) -- a checker/baseline, never the product
 # ---------------------------------------------------------------------------
-REF_DIR = os.path.join(REPO, "oracle", "_ref")
+REF_ZIP = os.path.join(REPO, "oracle", "_ref", "nfftkrr_ref.zip")
 _POOL = {}
 
 
 def import_reference():
     """The reference package byte-compiled by oracle/build_ref.py (prebuilt on the GPU box)."""
-    if not os.path.isdir(os.path.join(REF_DIR, "nfftkrr")):
+    if not os.path.exists(REF_ZIP):
         from oracle import build_ref
 
         if build_ref.build() is None:
-            raise RuntimeError("oracle/_ref/nfftkrr missing: run oracle/build_ref.py where "
-                               "/root/reference exists")
-    if REF_DIR not in sys.path:
-        sys.path.insert(0, REF_DIR)
+            raise RuntimeError("oracle/_ref/nfftkrr_ref.zip missing: run oracle/build_ref.py "
+                               "where /root/reference exists")
+    if REF_ZIP not in sys.path:
+        sys.path.insert(0, REF_ZIP)
     import nfftkrr
 
+    if not hasattr(nfftkrr, "FastsumOperator") or REF_ZIP not in (nfftkrr.__file__ or ""):
+        raise RuntimeError(f"imported {nfftkrr!r}, not the reference build in {REF_ZIP}")
     return nfftkrr
 
 

@@ -28,9 +28,13 @@
  *
  * Pointers: bulk arrays (coordinates, alpha, out, b, x) are DEVICE pointers on
  * desc->device; small parameter arrays are HOST pointers.  All arithmetic is
- * IEEE fp64.  A plan is immutable after creation; afs_apply / afs_cg_solve on
- * one plan are serialised internally (the plan owns one workspace), so they
- * are safe to call from several host threads.
+ * IEEE fp64.  A plan's geometry is immutable after creation.  afs_apply is
+ * reentrant: the first caller runs on the plan's own workspace,
+ * concurrent callers on up to 3 workspace clones (own grids, spectral scratch,
+ * streams and graphs; shared sorted nodes and multipliers), so applies from
+ * several host threads overlap on the device.  The stage-level entry points,
+ * afs_cg_solve and the mode setters use the plan's own workspace and are
+ * serialised with each other.
  */
 #ifndef ANOVAFS_H
 #define ANOVAFS_H

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <condition_variable>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -136,6 +137,15 @@ struct afs_plan {
   std::vector<double> win_ms_spread, win_ms_gather;    // accumulated, per window
   int64_t profiled_applies = 0;
   std::mutex mu;
+  // reentrant afs_apply (api.cu): concurrent callers beyond the first run on workspace
+  // clones -- plans that share this plan's immutable geometry (sorted sides, multipliers,
+  // coordinates, tables) and own their grids, scratch, limbs, streams and graphs
+  afs_plan* parent = nullptr;            // set on clones: nothing shared is freed with them
+  std::vector<afs_plan*> clones;
+  std::vector<char> clone_busy;
+  bool primary_busy = false;
+  std::mutex pool_mu;
+  std::condition_variable pool_cv;
 };
 
 namespace afs {

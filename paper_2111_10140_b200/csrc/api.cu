@@ -166,11 +166,15 @@ void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int6
 static void free_plan(afs_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  cudaFree(p->d_win);
-  cudaFree(p->src);
-  cudaFree(p->tgt);
-  cudaFree(p->mult);
-  cudaFree(p->twiddle);
+  for (afs_plan* c : p->clones) free_plan(c);
+  p->clones.clear();
+  if (!p->parent) {   // immutable parts: owned by the primary plan only
+    cudaFree(p->d_win);
+    cudaFree(p->src);
+    cudaFree(p->tgt);
+    cudaFree(p->mult);
+    cudaFree(p->twiddle);
+  }
   if (p->grids_owned) cudaFree(p->grids);
   if (p->spec_owned) cudaFree(p->spec);
   cudaFree(p->det_limbs);
@@ -200,12 +204,94 @@ static void free_plan(afs_plan* p) {
   }
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
-  for (SortedSide* s : p->src_side)
-    if (s) { free_sorted_side(s); delete s; }
-  for (SortedSide* s : p->tgt_side)
-    if (s) { free_sorted_side(s); delete s; }
-  delete p->poly;
+  if (!p->parent) {
+    for (SortedSide* s : p->src_side)
+      if (s) { free_sorted_side(s); delete s; }
+    for (SortedSide* s : p->tgt_side)
+      if (s) { free_sorted_side(s); delete s; }
+    delete p->poly;
+  }
   delete p;
+}
+
+void refresh_det_windows(afs_plan* p) {
+  for (Window& w : p->win) {
+    w.det_limbs = p->deterministic ? p->det_limbs : nullptr;
+    w.det_stride = p->grid_total * p->max_rhs;
+    w.det_scale = p->det_aux ? p->det_aux + 1 : nullptr;
+    w.det_base = p->grids;
+  }
+  for (GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  p->graphs.clear();
+  if (p->cg.graph.exec) cudaGraphExecDestroy(p->cg.graph.exec);   // so does the CG solve graph
+  p->cg.graph = CgGraph{};
+}
+
+// A workspace clone for a concurrent afs_apply: shares every immutable part of the plan,
+// owns the mutable ones (grids, spectral scratch, limbs, streams, captured graphs).
+static afs_plan* make_clone(afs_plan* p) {
+  afs_plan* c = new afs_plan();
+  try {
+    c->parent = p;
+    c->device = p->device;
+    c->P = p->P;
+    c->dtot = p->dtot;
+    c->Ns = p->Ns;
+    c->Nt = p->Nt;
+    c->has_targets = p->has_targets;
+    c->M = p->M; c->m = p->m; c->n = p->n; c->H = p->H;
+    c->b = p->b;
+    c->max_rhs = p->max_rhs;
+    c->win = p->win;
+    c->d_win = p->d_win;
+    c->src = p->src;
+    c->tgt = p->tgt;
+    c->mult = p->mult;
+    c->twiddle = p->twiddle;
+    c->grid_total = p->grid_total;
+    c->spec_total = p->spec_total;
+    c->scratch_a_len = p->scratch_a_len;
+    c->scratch_b_len = p->scratch_b_len;
+    c->launches_per_apply = p->launches_per_apply;
+    c->window_eval = p->window_eval;
+    c->kb_tab = p->kb_tab;
+    c->src_side = p->src_side;
+    c->tgt_side = p->tgt_side;
+    c->poly = p->poly;
+    c->use_graphs = p->use_graphs;
+    c->fft_mode = p->fft_mode;
+    c->stage_streams = p->stage_streams;
+    c->det_log2_bound = p->det_log2_bound;
+    c->deterministic = p->deterministic;
+    AFS_CUDA(cudaMalloc(&c->grids, sizeof(double) * c->grid_total * c->max_rhs));
+    if (c->scratch_a_len)
+      AFS_CUDA(cudaMalloc(&c->scratch_a, sizeof(double2) * c->scratch_a_len * c->max_rhs));
+    if (c->scratch_b_len)
+      AFS_CUDA(cudaMalloc(&c->scratch_b, sizeof(double2) * c->scratch_b_len * c->max_rhs));
+    if (c->deterministic) {
+      AFS_CUDA(cudaMalloc(&c->det_limbs, sizeof(long long) * 3 * (size_t)c->grid_total * c->max_rhs));
+      AFS_CUDA(cudaMalloc(&c->det_aux, 4 * sizeof(double)));
+    }
+    refresh_det_windows(c);
+  } catch (...) {
+    free_plan(c);
+    throw;
+  }
+  return c;
+}
+
+// Drops the clones (they copy the plan's mode at creation); waits for running applies.
+static void drop_clones(afs_plan* p) {
+  std::unique_lock<std::mutex> lk(p->pool_mu);
+  p->pool_cv.wait(lk, [p] {
+    for (char b : p->clone_busy)
+      if (b) return false;
+    return true;
+  });
+  for (afs_plan* c : p->clones) free_plan(c);
+  p->clones.clear();
+  p->clone_busy.clear();
 }
 
 static void create_plan(const afs_plan_desc* d, afs_plan** out) {
@@ -405,14 +491,13 @@ static void check_rhs(const afs_plan* plan, int32_t nrhs) {
   if (nrhs < 1 || nrhs > plan->max_rhs) throw afs::Error(AFS_ERR_SHAPE, "nrhs must lie in 1..max_rhs");
 }
 
-static void refresh_det_windows(afs_plan* p);
-
 int afs_spread(afs_plan* plan, const double* alpha, int64_t ld_alpha, int32_t nrhs, void* stream) {
   return afs::guarded([&] {
     check_rhs(plan, nrhs);
     if (!alpha || ld_alpha < plan->Ns) throw afs::Error(AFS_ERR_SHAPE, "bad alpha");
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
+    if (plan->ev_out) AFS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, plan->ev_out, 0));
     afs::spread_all(plan, alpha, ld_alpha, nrhs, (cudaStream_t)stream);
   });
 }
@@ -422,6 +507,7 @@ int afs_spectral(afs_plan* plan, int32_t nrhs, void* stream) {
     check_rhs(plan, nrhs);
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
+    if (plan->ev_out) AFS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, plan->ev_out, 0));
     afs::spectral_all(plan, nrhs, (cudaStream_t)stream);
   });
 }
@@ -440,6 +526,7 @@ int afs_spectral_forward(afs_plan* plan, int32_t nrhs, void* stream) {
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
     ensure_spectra(plan);
+    if (plan->ev_out) AFS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, plan->ev_out, 0));
     afs::spectral_all(plan, nrhs, (cudaStream_t)stream, 1);
   });
 }
@@ -450,6 +537,7 @@ int afs_spectral_inverse(afs_plan* plan, int32_t nrhs, void* stream) {
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
     if (!plan->spec) throw afs::Error(AFS_ERR_VALIDATION, "afs_spectral_inverse before forward");
+    if (plan->ev_out) AFS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, plan->ev_out, 0));
     afs::spectral_all(plan, nrhs, (cudaStream_t)stream, 2);
   });
 }
@@ -486,6 +574,7 @@ int afs_gather(afs_plan* plan, double* out, int64_t ld_out, int32_t nrhs, void* 
     if (!out || ld_out < plan->Nt) throw afs::Error(AFS_ERR_SHAPE, "bad out");
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
+    if (plan->ev_out) AFS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, plan->ev_out, 0));
     afs::gather_all(plan, out, ld_out, nrhs, (cudaStream_t)stream);
   });
 }
@@ -508,27 +597,15 @@ int afs_plan_bind_grids(afs_plan* plan, double* buffer, int64_t capacity_doubles
     if (plan->grids_owned) cudaFree(plan->grids);
     plan->grids = buffer;
     plan->grids_owned = false;
-    refresh_det_windows(plan);   // also drops captured graphs (they reference the old buffer)
+    afs::refresh_det_windows(plan);   // also drops captured graphs (they reference the old buffer)
   });
 }
 
-static void refresh_det_windows(afs_plan* p) {
-  for (afs::Window& w : p->win) {
-    w.det_limbs = p->deterministic ? p->det_limbs : nullptr;
-    w.det_stride = p->grid_total * p->max_rhs;
-    w.det_scale = p->det_aux ? p->det_aux + 1 : nullptr;
-    w.det_base = p->grids;
-  }
-  for (afs::GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  p->graphs.clear();
-  if (p->cg.graph.exec) cudaGraphExecDestroy(p->cg.graph.exec);   // so does the CG solve graph
-  p->cg.graph = afs::CgGraph{};
-}
 
 int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
   return afs::guarded([&] {
     if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
+    afs::drop_clones(plan);
     std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
     if (enable && plan->Ns > ((int64_t)1 << 27))
@@ -541,7 +618,7 @@ int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
       plan->device_bytes += (int64_t)bytes + 4 * (int64_t)sizeof(double);
     }
     plan->deterministic = enable != 0;
-    refresh_det_windows(plan);
+    afs::refresh_det_windows(plan);
   });
 }
 
@@ -549,6 +626,7 @@ int afs_plan_set_profiling(afs_plan* plan, int32_t enable) {
   return afs::guarded([&] {
     if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
     std::lock_guard<std::mutex> lock(plan->mu);
+    std::lock_guard<std::mutex> lk(plan->pool_mu);
     plan->profiling = enable != 0;
   });
 }
@@ -590,9 +668,72 @@ int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out
     if (!alpha || !out) throw afs::Error(AFS_ERR_SHAPE, "null alpha/out");
     if (ld_alpha < plan->Ns || ld_out < plan->Nt)
       throw afs::Error(AFS_ERR_SHAPE, "leading dimension smaller than vector length");
-    std::lock_guard<std::mutex> lock(plan->mu);
     AFS_CUDA(cudaSetDevice(plan->device));
-    afs::apply_impl(plan, alpha, ld_alpha, out, ld_out, nrhs, (cudaStream_t)stream);
+    // the first caller runs on the plan itself; concurrent callers take (or create, up to
+    // kMaxClones) a workspace clone, so applies on one plan overlap on the device
+    constexpr size_t kMaxClones = 3;
+    afs_plan* target = nullptr;
+    size_t slot = 0;
+    {
+      std::unique_lock<std::mutex> lk(plan->pool_mu);
+      for (;;) {
+        if (!plan->primary_busy) {
+          plan->primary_busy = true;
+          target = plan;
+          break;
+        }
+        if (plan->profiling) {   // per-stage timing lives on the plan: wait for it
+          plan->pool_cv.wait(lk);
+          continue;
+        }
+        for (slot = 0; slot < plan->clones.size(); ++slot)
+          if (!plan->clone_busy[slot]) break;
+        if (slot < plan->clones.size()) {
+          plan->clone_busy[slot] = 1;
+          target = plan->clones[slot];
+          break;
+        }
+        if (plan->clones.size() < kMaxClones) {
+          plan->clones.push_back(nullptr);
+          plan->clone_busy.push_back(1);
+          slot = plan->clones.size() - 1;
+          lk.unlock();
+          afs_plan* c = nullptr;
+          try {
+            c = afs::make_clone(plan);
+          } catch (...) {
+            lk.lock();
+            plan->clones.erase(plan->clones.begin() + slot);
+            plan->clone_busy.erase(plan->clone_busy.begin() + slot);
+            plan->pool_cv.notify_all();
+            throw;
+          }
+          lk.lock();
+          plan->clones[slot] = c;
+          target = c;
+          break;
+        }
+        plan->pool_cv.wait(lk);
+      }
+    }
+    auto release = [&] {
+      std::lock_guard<std::mutex> lk(plan->pool_mu);
+      if (target == plan) plan->primary_busy = false;
+      else plan->clone_busy[slot] = 0;
+      plan->pool_cv.notify_all();
+    };
+    try {
+      if (target == plan) {
+        std::lock_guard<std::mutex> lock(plan->mu);   // vs the stage-level entry points
+        afs::apply_impl(plan, alpha, ld_alpha, out, ld_out, nrhs, (cudaStream_t)stream);
+      } else {
+        afs::apply_impl(target, alpha, ld_alpha, out, ld_out, nrhs, (cudaStream_t)stream);
+      }
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
   });
 }
 

@@ -8,6 +8,7 @@
 namespace afs {
 
 #include "kb_tables.inc"
+#include "kb_cheb.inc"
 
 constexpr int kPolyMaxOffsets = 2 * AFS_MAX_CUTOFF;   // 2m
 constexpr int kPolyTerms = 14;                        // degree 13 in x = f - 1/4

@@ -60,9 +60,39 @@ void spread_tc(const SortedSide& sv, const Window& w, int n, const double* alpha
     launch(k_spread_tc<RG, TAB, kU, false, kD>);
 }
 
+// AFS_CHEB=0 selects the DMMA gather (k_gather_tc) for one right-hand side too (A/B hook)
+bool cheb_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("AFS_CHEB");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <int TAB>
+void gather_cheb(const SortedSide& sv, const Window& w, int n, const double* grid, double* out,
+                 cudaStream_t s) {
+  const int64_t ng = sv.ngroups;
+  auto launch = [&](auto kernel) {
+    static int wps = 0;
+    if (wps == 0) wps = tc_warps_per_sm(kernel);
+    const int gpw = groups_per_warp(ng, wps);
+    const int64_t warps = (ng + gpw - 1) / gpw;
+    const int64_t blocks = (warps * 32 + 127) / 128;
+    kernel<<<(unsigned)blocks, 128, 0, s>>>(sv, w, n, grid, out, gpw);
+  };
+  if (pow2(n))
+    launch(k_gather_cheb<TAB, true, kD>);
+  else
+    launch(k_gather_cheb<TAB, false, kD>);
+}
+
 template <int RG, int TAB>
 void gather_tc(const SortedSide& sv, const Window& w, int n, const double* grid, int64_t rs, int nr,
                double* out, int64_t ldo, cudaStream_t s) {
+  static_assert(kU == 4, "the Chebyshev gather takes batches of 4 groups");
+  if (RG == 1 && nr == 1 && cheb_enabled()) return gather_cheb<TAB>(sv, w, n, grid, out, s);
   const int64_t ng = sv.ngroups;
   auto launch = [&](auto kernel) {
     static int wps = 0;

@@ -30,6 +30,9 @@
 #ifndef AFS_TC_MINB_SPREAD
 #define AFS_TC_MINB_SPREAD 1
 #endif
+#ifndef AFS_TC_MINB_CHEB
+#define AFS_TC_MINB_CHEB 4
+#endif
 
 #include "geometry.cuh"
 #include "sliding.cuh"
@@ -363,6 +366,201 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_GATHER : 1) k_gathe
       const double sum = (b1 ? v1 : v0) + __shfl_xor_sync(0xffffffffu, b1 ? v0 : v1, 2);
       if (j >= 0 && r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, sum));
     }
+    st = st1;
+  }
+  cp_async_wait<0>();
+}
+
+// ----------------------------------------------------------------------------
+// gather, one right-hand side, Chebyshev-folded (k_gather_cheb).
+//
+// Per half-cell the 8x8 grid window G (stencil offsets in polynomial order, reflection
+// folded into the addressing) and both dimensions' window polynomials fold into ONE
+// bivariate Chebyshev series
+//     s(x, y) = sum_{a,b} G[a][b] P_a(x) P_b(y) = sum_{k,l} Ghat[k][l] T_k(4x) T_l(4y),
+//     Ghat = Cc^T G Cc    (Cc: kb_cheb.inc, the same 12-term interpolants as kb_tables.inc)
+// whose coefficients decay like the product of the 1-D ones, so the terms with k + l > 14
+// are below 1e-16 of the window scale and are dropped: 104 coefficients instead of 144
+// (packed rows of 12,12,12,12,10,10,8,8,6,6,4,4).  A node then costs 136 DFMAs (two
+// 11-step Chebyshev recurrences + 104 coefficient FMAs + 12) against the 1536 DMMA MACs +
+// power products per 8 nodes of k_gather_tc; the fold is 10 DMMAs per half-cell and warp.
+// Lane = node (32 nodes = 4 groups per batch); the coefficients are broadcast from a
+// per-warp shared-memory table ring.
+// ----------------------------------------------------------------------------
+constexpr int kChebTab = 104;          // packed coefficients per half-cell
+constexpr int kChebSlots = 5;          // tables per warp: 4 new per batch + the live one
+
+__host__ __device__ constexpr int cheb_rowlen(int k) { return k < 4 ? 12 : 12 - 2 * ((k - 2) / 2); }
+__host__ __device__ constexpr int cheb_off(int k) {
+  int o = 0;
+  for (int j = 0; j < k; ++j) o += cheb_rowlen(j);
+  return o;
+}
+
+template <int TAB, bool POW2, int D>
+__global__ void __launch_bounds__(128, AFS_TC_MINB_CHEB) k_gather_cheb(
+    const SortedSide sv, const Window w, int n, const double* __restrict__ grid,
+    double* __restrict__ out, int gpw) {
+  constexpr int U = 4;
+  static_assert(D >= 4, "values are staged two batches ahead of node data landing");
+  __shared__ TcRing<U, D, 1> ring[4];
+  __shared__ __align__(16) double tabs[4][kChebSlots][kChebTab];
+  const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
+  const int wib = threadIdx.x >> 5;
+  TcRing<U, D, 1>& R = ring[wib];
+  double* tab = &tabs[wib][0][0];
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g0 = warp * gpw;
+  if (g0 >= sv.ngroups) return;   // warp-uniform
+  const int g1 = min(g0 + gpw, (int)sv.ngroups);
+  const double* g = grid + w.grid_off;
+
+  // fold constants.  Step 1 (H^T = Cc^T G^T): A[l = slot + 8 mb][b = q + 4 s] = Cc[b][l];
+  // step 2 (Ghat^T = H^T Cc, k relabelled a = 2q + e): B[a = 2q + e][k = slot + 8 nb] = Cc[a][k]
+  double ca[2][2], cb[2][2];
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int l = slot + 8 * mb, b = q + 4 * s2;
+      const double c = l < 12 ? kb_cheb<TAB>(b, l) : 0.0;
+      asm volatile("mov.b64 %0, %1;" : "=d"(ca[mb][s2]) : "d"(c));
+      const int k = slot + 8 * mb, a = 2 * q + s2;
+      const double c2 = k < 12 ? kb_cheb<TAB>(a, k) : 0.0;
+      asm volatile("mov.b64 %0, %1;" : "=d"(cb[mb][s2]) : "d"(c2));
+    }
+  // packed store index of the lane's fold outputs: block (mb, nb) in {(0,0), (0,1), (1,0)},
+  // element e: Ghat^T[l = slot + 8 mb][k = 2q + e + 8 nb]; -1 when not kept
+  int sidx[3][2];
+#pragma unroll
+  for (int bi = 0; bi < 3; ++bi)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int mb = bi == 2 ? 1 : 0, nb = bi == 1 ? 1 : 0;
+      const int l = slot + 8 * mb, k = 2 * q + e + 8 * nb;
+      sidx[bi][e] = (k < 12 && l < cheb_rowlen(k)) ? cheb_off(k) + l : -1;
+    }
+
+  // fold inputs of one batch, loaded one batch ahead for the groups whose header changes:
+  // gw[u][s] = G[a = slot][b = q + 4 s] of group u's half-cell
+  int32_t hlast = -1;
+  auto load_fold = [&](int st, double (&gw)[U][2], unsigned& chg) {
+    chg = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t h = R.hdr[st][u];
+      if (h != hlast) {   // warp-uniform
+        const int row = tc_cell<POW2>(tc_u0(h), tc_c0(h), slot, n) * n;
+        gw[u][0] = __ldg(g + row + tc_cell<POW2>(tc_u1(h), tc_c1(h), q, n));
+        gw[u][1] = __ldg(g + row + tc_cell<POW2>(tc_u1(h), tc_c1(h), q + 4, n));
+        hlast = h;
+        chg |= 1u << u;
+      }
+    }
+  };
+  auto fold = [&](const double (&gv)[2], double* dst) {
+    double ht[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      dmma884(ht[mb], ca[mb][0], gv[0]);
+      dmma884(ht[mb], ca[mb][1], gv[1]);
+    }
+    double gt[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      dmma884(gt[0], ht[0][e], cb[0][e]);
+      dmma884(gt[1], ht[0][e], cb[1][e]);
+      dmma884(gt[2], ht[1][e], cb[0][e]);
+    }
+#pragma unroll
+    for (int bi = 0; bi < 3; ++bi)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (sidx[bi][e] >= 0) dst[sidx[bi][e]] = gt[bi][e];
+  };
+
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    tc_stage_nodes(R, k, sv, g0 + k * U, lane);
+    cp_async_commit();
+  }
+  cp_async_wait<D - 2>();
+  __syncwarp();
+  tc_stage_vals(R, 0, out, 0, 1, lane);
+  tc_stage_vals(R, 1, out, 0, 1, lane);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  double gnext[U][2];
+  unsigned chg_next;
+  load_fold(0, gnext, chg_next);   // hlast = -1: the first group loads
+  int live = 0;                     // table slot of the previous batch's last group
+  int st = 0;
+  const int ug = lane >> 3;
+#pragma unroll 1
+  for (int gb = g0; gb < g1; gb += U) {
+    cp_async_wait<1>();   // node data up to batch b + 2 and values of batch b have landed
+    __syncwarp();         // (also: every lane is done reading the previous batch's tables)
+    const double u4 = 4.0 * R.x0[st][lane];
+    const double v4 = 4.0 * R.x1[st][lane];
+    const int j = R.perm[st][lane];
+    const double prior = R.val[st][0][lane];
+    double gcur[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) gcur[u][0] = gnext[u][0], gcur[u][1] = gnext[u][1];
+    const unsigned chg = chg_next;
+    const int st1 = st + 1 == D ? 0 : st + 1;
+    const int st2 = st1 + 1 == D ? 0 : st1 + 1;
+    __syncwarp();
+    tc_stage_nodes(R, st, sv, gb + D * U, lane);   // refill the slot just read
+    tc_stage_vals(R, st2, out, 0, 1, lane);         // values of batch b + 2
+    cp_async_commit();
+    load_fold(st1, gnext, chg_next);                // fold inputs of batch b + 1
+    // tables of this batch's new half-cells go to the slots other than the live one
+    int ts[U];
+    int cur = live, nnew = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (chg & (1u << u)) {   // warp-uniform
+        cur = nnew < live ? nnew : nnew + 1;
+        ++nnew;
+        fold(gcur[u], tab + cur * kChebTab);
+      }
+      ts[u] = cur;
+    }
+    live = cur;
+    __syncwarp();
+    const double* T = tab + (ug == 0 ? ts[0] : ug == 1 ? ts[1] : ug == 2 ? ts[2] : ts[3]) * kChebTab;
+    // Chebyshev values of y, then the rows k of the table against them, outer recurrence in x
+    double ty[12];
+    ty[0] = 1.0;
+    ty[1] = v4;
+    const double v8 = 2.0 * v4;
+#pragma unroll
+    for (int l = 2; l < 12; ++l) ty[l] = fma(v8, ty[l - 1], -ty[l - 2]);
+    const double u8 = 2.0 * u4;
+    double tkm1 = 1.0, tk = 1.0, s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      if (k == 1) {
+        tkm1 = 1.0;
+        tk = u4;
+      } else if (k >= 2) {
+        const double tn = fma(u8, tk, -tkm1);
+        tkm1 = tk;
+        tk = tn;
+      }
+      const double* row = T + cheb_off(k);
+      double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < cheb_rowlen(k); l += 2) {
+        const double2 c = *reinterpret_cast<const double2*>(row + l);
+        p0 = fma(c.x, ty[l], p0);
+        p1 = fma(c.y, ty[l + 1], p1);
+      }
+      s = fma(tk, p0 + p1, s);
+    }
+    if (j >= 0) out[j] = __dadd_rn(prior, __dmul_rn(w.eta, s));
     st = st1;
   }
   cp_async_wait<0>();

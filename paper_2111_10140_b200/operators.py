@@ -247,8 +247,16 @@ class _Plan:
         _native.check(self.lib.afs_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
         self.handle = handle
         del Xd, Zd
-        self._lock = threading.Lock()
-        self._stage = {}
+        self._tls = threading.local()   # per-thread staging: applies are reentrant (api.cu)
+
+    def _staging(self, key, make):
+        """This thread's host/device staging buffers for `key` (created on first use)."""
+        st = getattr(self._tls, "stage", None)
+        if st is None:
+            st = self._tls.stage = {}
+        if key not in st:
+            st[key] = make()
+        return st[key]
 
     def info(self):
         inf = _native.PlanInfo()
@@ -385,35 +393,31 @@ class _Plan:
         R = 1 if one else arr.shape[1]
         if R > self.max_rhs:
             raise ShapeError(f"at most {self.max_rhs} right-hand sides per apply")
-        with self._lock:
-            st = self._stage.get(R)
-            if st is None:
-                st = (torch.empty((R, self.N), dtype=torch.float64, pin_memory=True),
-                      torch.empty((R, self.N), dtype=torch.float64, device=self.device),
-                      torch.empty((R, self.Nt), dtype=torch.float64, device=self.device),
-                      torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=True))
-                self._stage[R] = st
-            h_in, d_in, d_out, h_out = st
-            stream = torch.cuda.current_stream(self.device)
-            src = torch.from_numpy(np.ascontiguousarray(arr.T) if not one else arr)
-            src = src[None, :] if one else src
-            # chunked host->pinned (multi-threaded torch copy) overlapped with async H2D
-            for lo, hi in _chunks(self.N):
-                h_in[:, lo:hi].copy_(src[:, lo:hi])
-                d_in[:, lo:hi].copy_(h_in[:, lo:hi], non_blocking=True)
-            self.apply_device(d_in, d_out, R)
-            res = np.empty((R, self.Nt))
-            dst = torch.from_numpy(res)
-            events = []
-            for lo, hi in _chunks(self.Nt):
-                h_out[:, lo:hi].copy_(d_out[:, lo:hi], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(stream)
-                events.append((lo, hi, ev))
-            for lo, hi, ev in events:   # pinned->host copy of chunk k overlaps D2H of k+1..
-                ev.synchronize()
-                dst[:, lo:hi].copy_(h_out[:, lo:hi])
-            return res[0] if one else res.T
+        h_in, d_in, d_out, h_out = self._staging(R, lambda: (
+            torch.empty((R, self.N), dtype=torch.float64, pin_memory=True),
+            torch.empty((R, self.N), dtype=torch.float64, device=self.device),
+            torch.empty((R, self.Nt), dtype=torch.float64, device=self.device),
+            torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=True)))
+        stream = torch.cuda.current_stream(self.device)
+        src = torch.from_numpy(np.ascontiguousarray(arr.T) if not one else arr)
+        src = src[None, :] if one else src
+        # chunked host->pinned (multi-threaded torch copy) overlapped with async H2D
+        for lo, hi in _chunks(self.N):
+            h_in[:, lo:hi].copy_(src[:, lo:hi])
+            d_in[:, lo:hi].copy_(h_in[:, lo:hi], non_blocking=True)
+        self.apply_device(d_in, d_out, R)
+        res = np.empty((R, self.Nt))
+        dst = torch.from_numpy(res)
+        events = []
+        for lo, hi in _chunks(self.Nt):
+            h_out[:, lo:hi].copy_(d_out[:, lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            events.append((lo, hi, ev))
+        for lo, hi, ev in events:   # pinned->host copy of chunk k overlaps D2H of k+1..
+            ev.synchronize()
+            dst[:, lo:hi].copy_(h_out[:, lo:hi])
+        return res[0] if one else res.T
 
     def _apply_host_tensor(self, alpha):
         """torch CPU tensor in -> torch CPU tensor out.  From pinned memory the H2D copy is
@@ -428,26 +432,21 @@ class _Plan:
             raise ShapeError(f"at most {self.max_rhs} right-hand sides per apply")
         a = alpha.to(torch.float64)
         pinned = a.is_pinned()
-        with self._lock:
-            key = ("tensor", R)
-            st = self._stage.get(key)
-            if st is None:
-                st = (torch.empty((self.N, R), dtype=torch.float64, device=self.device),
-                      torch.empty((R, self.N), dtype=torch.float64, device=self.device),
-                      torch.empty((R, self.Nt), dtype=torch.float64, device=self.device))
-                self._stage[key] = st
-            d_raw, d_in, d_out = st
-            stream = torch.cuda.current_stream(self.device)
-            if one:
-                d_in[0].copy_(a, non_blocking=pinned)
-            else:   # (N, R) row-major on the host: copy as is, transpose on the device
-                d_raw.copy_(a.contiguous(), non_blocking=pinned)
-                d_in.copy_(d_raw.t())
-            self.apply_device(d_in, d_out, R)
-            res = torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=pinned)
-            res.copy_(d_out, non_blocking=pinned)
-            stream.synchronize()
-            return res[0] if one else res.t()
+        d_raw, d_in, d_out = self._staging(("tensor", R), lambda: (
+            torch.empty((self.N, R), dtype=torch.float64, device=self.device),
+            torch.empty((R, self.N), dtype=torch.float64, device=self.device),
+            torch.empty((R, self.Nt), dtype=torch.float64, device=self.device)))
+        stream = torch.cuda.current_stream(self.device)
+        if one:
+            d_in[0].copy_(a, non_blocking=pinned)
+        else:   # (N, R) row-major on the host: copy as is, transpose on the device
+            d_raw.copy_(a.contiguous(), non_blocking=pinned)
+            d_in.copy_(d_raw.t())
+        self.apply_device(d_in, d_out, R)
+        res = torch.empty((R, self.Nt), dtype=torch.float64, pin_memory=pinned)
+        res.copy_(d_out, non_blocking=pinned)
+        stream.synchronize()
+        return res[0] if one else res.t()
 
 
 class AnovaKernelOperator:
@@ -537,6 +536,10 @@ class FastsumOperator:
         self.dims = d
         self._plan = _Plan(X, Z, [tuple(range(d))], [1.0], kernel, config, profile, device, max_rhs,
                            window_eval)
+        self._nodes = (X, Z)             # for the lazily built NfftPlan views
+        self._nfft = {}
+        self._device = device
+        self._window_eval = window_eval
         if deterministic:
             self._plan.set_deterministic(True)
         w = self._plan.windows[0]
@@ -558,6 +561,43 @@ class FastsumOperator:
         if a.shape[0] != self.n_sources or len(a.shape) not in (1, 2):
             raise ShapeError(f"alpha must have length {self.n_sources}, got shape {tuple(a.shape)}")
         return self._plan.apply(a)
+
+    # -- the reference's NFFT-level view of the operator (fastsum.py:228-252) ----------
+    def _nfft_plan(self, side):
+        """GPU NfftPlan on the scaled sources / targets, built on first use: the nodes are
+        (x - center) * scale exactly as fastsum.py:228-232 forms them."""
+        if side not in self._nfft:
+            from .nfft import NfftPlan
+            from .params import GridSpec
+
+            A = self._nodes[0 if side == "source" else 1]
+            if A is None:
+                self._nfft[side] = None
+            else:
+                A = A.cpu().numpy() if hasattr(A, "is_cuda") else A
+                grid = GridSpec((self.config.coeff_grid,) * self.dims)
+                self._nfft[side] = NfftPlan(grid, (A - self.center) * self.scale, self.profile,
+                                            device=self._device, window_eval=self._window_eval)
+        return self._nfft[side]
+
+    @property
+    def source_plan(self):
+        return self._nfft_plan("source")
+
+    @property
+    def target_plan(self):
+        return self._nfft_plan("target")
+
+    def apply_complex(self, alpha):
+        """forward_Z(c_hat * adjoint_X(alpha)) for real or complex alpha, without taking the
+        real part (fastsum.py:243-252): the NFFT stages run on the GPU, the M^d spectrum
+        product and the Hermitian folding on the host.  ``apply`` is the fused real path."""
+        a = np.asarray(alpha)
+        if a.ndim != 1 or a.shape[0] != self.n_sources:
+            raise ShapeError(f"alpha must have length {self.n_sources}, got shape {a.shape}")
+        spectrum = self.source_plan.adjoint(a.astype(np.complex128, copy=False))
+        out_plan = self.target_plan if self.target_plan is not None else self.source_plan
+        return out_plan.forward(self.coeffs.ravel() * spectrum)
 
 
 def fastsum_build(kernel, config, sources, targets=None, profile="default", **kw):

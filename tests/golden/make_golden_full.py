@@ -9,6 +9,7 @@ Run in the build container (where /root/reference exists), one job per process
     python tests/golden/make_golden_full.py c4      # N=1M, R=8 one 3-D window
     python tests/golden/make_golden_full.py c5      # N=1M composed 30-window matvec
     python tests/golden/make_golden_full.py c5cg    # C5 recipe CG at N=2000/8000 (converges)
+    python tests/golden/make_golden_full.py complex # FastsumOperator.apply_complex cases
 
 Inputs are regenerated from seeds (``paper_2111_10140_b200.synthetic``) on both
 sides; only outputs are stored.  Vectors up to 1M entries are stored whole
@@ -131,6 +132,19 @@ def job_c5cg():
         t0 = time.time()
         res = cg_solve(lambda v: _composed(ops, v) + w.beta * v, w.y, tol=1e-6, maxiter=1000)
         tight = cg_solve(lambda v: _composed(ops, v) + w.beta * v, w.y, tol=1e-11, maxiter=2000)
+        # the reference's own roundoff sensitivity: the same recipe with the windows summed in
+        # other orders (reverse + 3 seeded permutations; equally valid compositions whose
+        # matvecs differ by ~1e-16)
+        orders = [list(range(len(ops)))[::-1]] + [
+            list(np.random.default_rng(100 + k).permutation(len(ops))) for k in range(3)]
+        for k, order in enumerate(orders):
+            perm_ops = [ops[i] for i in order]
+            pert = cg_solve(lambda v: _composed(perm_ops, v) + w.beta * v, w.y, tol=1e-6,
+                            maxiter=1000)
+            g[f"n{N}_x_pert{k}"] = pert.x
+            g[f"n{N}_iters_pert{k}"] = np.array(pert.iterations)
+            print(N, "perturbation", k, pert.iterations,
+                  np.linalg.norm(pert.x - res.x) / np.linalg.norm(res.x), flush=True)
         print(N, res.iterations, res.residual, tight.iterations, tight.residual,
               time.time() - t0, flush=True)
         g[f"n{N}_x"] = res.x
@@ -144,8 +158,24 @@ def job_c5cg():
     _save("golden_c5cg.npz", **g)
 
 
+def job_complex():
+    """FastsumOperator.apply_complex (fastsum.py:243-252) on real and complex alpha."""
+    from cases import FASTSUM_CASES, fastsum_inputs
+
+    g = {}
+    for tag, d, M, m, os_, sigma, N, n_tgt in FASTSUM_CASES[:7]:
+        X, Z, alpha = fastsum_inputs(tag, d, N, n_tgt)
+        op = FastsumOperator(GaussianKernel(sigma), PeriodizationConfig(coeff_grid=M), X, Z,
+                             AccuracyProfile("golden", os_, m))
+        calpha = alpha + 1j * np.random.default_rng(len(tag)).standard_normal(N)
+        g[tag + "_real"] = op.apply_complex(alpha)
+        g[tag + "_cplx"] = op.apply_complex(calpha)
+    g["meta_json"] = _meta(job="complex")
+    _save("golden_complex.npz", **g)
+
+
 JOBS = {"c2": job_c2, "c2cg50": lambda: job_c2(50, "c2cg50"), "c3": job_c3, "c4": job_c4,
-        "c5": job_c5, "c5cg": job_c5cg}
+        "c5": job_c5, "c5cg": job_c5cg, "complex": job_complex}
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or JOBS:

@@ -114,17 +114,19 @@ def test_point_sharded_cuda_two_ranks(tmp_path, exchange):
     assert err < 1e-13
 
 
-def _c5_small():
+def _c2_small():
+    """The C2 recipe (3 windows, beta=1): well conditioned, so single- and two-rank solves
+    that differ only by the order of cross-window additions stay within roundoff."""
     from paper_2111_10140_b200 import synthetic
 
-    return synthetic.c5(N=8000)
+    return synthetic.c2(N=20_000, n_test=10)
 
 
 def _cg_window_worker(rank, world, port, out):
     torch, dist = _init(rank, world, port)
     import paper_2111_10140_b200 as afs
 
-    w = _c5_small()
+    w = _c2_small()
     op = afs.WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, device=0)
     res = afs.cg_solve(afs.KernelSystem(op, w.beta), torch.from_numpy(w.y).cuda(), 1e-6, 1000)
     np.save(f"{out}.{rank}.npy", np.concatenate([[res.iterations, res.residual],
@@ -139,7 +141,7 @@ def test_window_sharded_cg_two_ranks(tmp_path):
 
     out = str(tmp_path / "wcg")
     _run(_cg_window_worker, out)
-    w = _c5_small()
+    w = _c2_small()
     op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m), None,
                                  afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
                                  deterministic=True)
@@ -161,7 +163,7 @@ def _cg_point_worker(rank, world, port, out):
     y = np.sin(7.0 * w.X).sum(axis=1)
     shard = np.array_split(np.arange(w.N), world)[rank]
     be = CudaPointBackend(w.X[shard], [(0, 1, 2)], w.sigma, M=w.M, m=w.m, device=0)
-    sys_ = afs.KernelSystem(afs.PointSharded(be), 0.5)
+    sys_ = afs.KernelSystem(afs.PointSharded(be), 50.0)
     res = afs.cg_solve(sys_, torch.from_numpy(y[shard].copy()).cuda(), 1e-8, 500)
     np.save(f"{out}.{rank}.npy", np.concatenate([[res.iterations, res.residual],
                                                  res.x.cpu().numpy()]))
@@ -170,7 +172,8 @@ def _cg_point_worker(rank, world, port, out):
 
 def test_point_sharded_cg_two_ranks(tmp_path):
     """Row-sharded CG with scalar all-reduces: the stacked shards equal the single-rank
-    solve at the same iteration count."""
+    solve at the same iteration count (beta = 50 keeps the clustered C4 system well
+    conditioned, so roundoff-level differences are not amplified)."""
     import paper_2111_10140_b200 as afs
 
     out = str(tmp_path / "pcg")
@@ -179,7 +182,7 @@ def test_point_sharded_cg_two_ranks(tmp_path):
     y = np.sin(7.0 * w.X).sum(axis=1)
     op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m), None,
                                  afs.PeriodizationConfig(coeff_grid=w.M), strict=False)
-    ref = afs.cg_solve(afs.KernelSystem(op, 0.5), y, 1e-8, 500)
+    ref = afs.cg_solve(afs.KernelSystem(op, 50.0), y, 1e-8, 500)
     parts = [np.load(f"{out}.{r}.npy") for r in range(2)]
     assert parts[0][0] == parts[1][0] and parts[0][1] == parts[1][1]
     x = np.concatenate([p[2:] for p in parts])
