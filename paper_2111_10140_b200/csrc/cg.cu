@@ -14,6 +14,9 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <algorithm>
+#include <cooperative_groups.h>
+
 #include "afs_internal.cuh"
 
 namespace afs {
@@ -162,6 +165,129 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_dir_dev(double* __restrict__
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
+// ---- the whole CG epilogue of one iteration in one cooperative launch -----------------------
+// Phase 1: Ap += beta p (Ap holds K p from the matvec), block partials of p.Ap, non-finite
+// flag; grid sync; phase 2: every block reduces the partials in the same fixed order (so all
+// hold the same pAp), x += (rs/pAp) p, r -= (rs/pAp) Ap, partials of r.r; grid sync; phase 3:
+// every block reduces rs_new, block 0 applies the reference's checks (k_cg_decide's logic)
+// and ends the WHILE loop, and while running every block updates p = r + (rs_new/rs) p.
+// Replaces k_cg_ap + k_finish + k_cg_update_dev + k_finish + k_cg_decide + k_cg_dir_dev
+// (six launches and one vector pass) in the whole-solve graph.  Values are bit-identical
+// to the unfused kernels: the same per-element expressions and the same reduction order.
+__device__ __forceinline__ double grid_partials_sum(const double* __restrict__ part, int np) {
+  __shared__ double bcast;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) v += part[i];
+  v = block_sum(v);
+  if (threadIdx.x == 0) bcast = v;
+  __syncthreads();
+  const double r = bcast;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_cg_fused(double* __restrict__ x, double* __restrict__ r,
+                                                         double* __restrict__ p, double* __restrict__ ap,
+                                                         double* __restrict__ ds, int64_t n,
+                                                         double* __restrict__ part1,
+                                                         double* __restrict__ part2,
+                                                         cudaGraphConditionalHandle h) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x;
+  const double beta = ds[9], rs = ds[0], it_prev = ds[4], bar = ds[6], maxit = ds[7];
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)G * blockDim.x;
+  {   // phase 1 (k_cg_ap)
+    double v = 0.0;
+    bool bad = false;
+    for (int64_t i = i0; i < n; i += stride) {
+      const double pi = p[i];
+      const double a = __dadd_rn(ap[i], __dmul_rn(beta, pi));
+      bad |= !isfinite(a);
+      ap[i] = a;
+      v += pi * a;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) ds[3] = 1.0;
+    v = block_sum(v);
+    if (threadIdx.x == 0) part1[blockIdx.x] = v;
+  }
+  grid.sync();
+  const double pAp = grid_partials_sum(part1, G);
+  {   // phase 2 (k_cg_update_dev)
+    const double step = rs / pAp;
+    double v = 0.0;
+    for (int64_t i = i0; i < n; i += stride) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(step, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(step, ap[i]));
+      r[i] = ri;
+      v += ri * ri;
+    }
+    v = block_sum(v);
+    if (threadIdx.x == 0) part2[blockIdx.x] = v;
+  }
+  grid.sync();
+  const double rs_new = grid_partials_sum(part2, G);
+  // phase 3 (k_cg_decide + k_cg_dir_dev); every block reaches the same status
+  const double it = it_prev + 1.0;
+  int status = kCgRunning;
+  if (ds[3] != 0.0) status = kCgBadAp;
+  else if (!isfinite(pAp) || pAp <= 0.0) status = kCgBadCurv;
+  else if (!isfinite(rs_new)) status = kCgBadRes;
+  else if (sqrt(rs_new) <= bar) status = kCgConverged;
+  else if (it >= maxit) status = kCgMaxiter;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ds[1] = pAp;
+    ds[2] = rs_new;
+    ds[4] = it;
+    if (status >= 0) {
+      ds[8] = rs_new / rs;
+      ds[0] = rs_new;
+    }
+    ds[5] = (double)status;
+    cudaGraphSetConditional(h, status == kCgRunning ? 1u : 0u);
+  }
+  if (status == kCgRunning) {
+    const double b2 = rs_new / rs;
+    for (int64_t i = i0; i < n; i += stride) p[i] = __dadd_rn(r[i], __dmul_rn(b2, p[i]));
+  }
+}
+
+// grid of the fused kernel: kRedBlocks when that many blocks are co-resident (cooperative
+// launch requirement), else the largest co-resident count -- fixed per device, so the
+// reduction order (hence the results) is fixed too
+static int cg_fused_grid() {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, occ = 0, coop = 0;
+    AFS_CUDA(cudaGetDevice(&dev));
+    AFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    AFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    AFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cg_fused, kRedThreads, 0));
+    grid = coop ? std::min(kRedBlocks, occ * sms) : -1;
+  }
+  return grid;
+}
+
+static void launch_cg_fused(afs_plan* pl, double* x, double* ds, cudaGraphConditionalHandle h,
+                            cudaStream_t s) {
+  CgScratch& c = pl->cg;
+  const int64_t n = pl->Ns;
+  double* part1 = c.partial;
+  double* part2 = c.partial + kRedBlocks;
+  void* args[] = {&x, &c.r, &c.p, &c.ap, &ds, (void*)&n, &part1, &part2, &h};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cg_fused_grid());
+  cfg.blockDim = dim3(kRedThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AFS_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k_cg_fused, args));
+}
+
 // ---- CG vector kernels on caller-owned vectors (afs_cg_vec_*, distributed drivers) --------
 // ws (caller-owned device doubles, AFS_CG_WORKSPACE_DOUBLES): [0] rs  [1] pAp  [2] rs_new
 // [3] non-finite flag  [9] beta  [16..16+kRedBlocks) reduction partials.  Every value
@@ -244,11 +370,11 @@ static void ensure_cg(afs_plan* pl) {
   AFS_CUDA(cudaMalloc(&c.p, bytes));
   AFS_CUDA(cudaMalloc(&c.ap, bytes));
   AFS_CUDA(cudaMalloc(&c.x, bytes));
-  AFS_CUDA(cudaMalloc(&c.partial, sizeof(double) * kRedBlocks));
+  AFS_CUDA(cudaMalloc(&c.partial, sizeof(double) * 2 * kRedBlocks));
   AFS_CUDA(cudaMalloc(&c.scalars, sizeof(double) * 16));
   AFS_CUDA(cudaMallocHost(&c.host_scalars, sizeof(double) * 16));
   c.n = pl->Ns;
-  pl->device_bytes += 4 * bytes + sizeof(double) * (kRedBlocks + 16);
+  pl->device_bytes += 4 * bytes + sizeof(double) * (2 * kRedBlocks + 16);
 }
 
 // Builds (once per plan) the whole-loop graph.  It works on plan-owned vectors only (x, r,
@@ -286,12 +412,17 @@ static bool cg_graph(afs_plan* pl, const double* b, cudaStream_t s) {
   AFS_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
     apply_stages(pl, c.p, n, c.ap, n, 1, s);
-    k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, ds + 9, n, c.partial, ds + 3);
-    k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 1);
-    k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.ap, ds, n, c.partial);
-    k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 2);
-    k_cg_decide<<<1, 1, 0, s>>>(ds, h);
-    k_cg_dir_dev<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.r, ds, n);
+    const char* fz = getenv("AFS_CG_FUSED");
+    if (cg_fused_grid() > 0 && !(fz && fz[0] == '0')) {
+      launch_cg_fused(pl, x, ds, h, s);   // the whole epilogue in one cooperative launch
+    } else {
+      k_cg_ap<<<kRedBlocks, kRedThreads, 0, s>>>(c.ap, c.p, ds + 9, n, c.partial, ds + 3);
+      k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 1);
+      k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.ap, ds, n, c.partial);
+      k_finish<<<1, kRedThreads, 0, s>>>(c.partial, kRedBlocks, ds + 2);
+      k_cg_decide<<<1, 1, 0, s>>>(ds, h);
+      k_cg_dir_dev<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.r, ds, n);
+    }
   } catch (...) {
     cudaStreamEndCapture(s, &body);
     cudaGraphDestroy(g);

