@@ -42,9 +42,38 @@ int groups_per_warp(int64_t ngroups, int warps_per_sm) {
 
 bool pow2(int n) { return (n & (n - 1)) == 0; }
 
+template <int TAB>
+void spread_cheb(const SortedSide& sv, const Window& w, int n, const double* alpha, double* grid,
+                 cudaStream_t s) {
+  const int64_t ng = sv.ngroups;
+  auto launch = [&](auto kernel) {
+    static int wps = 0;
+    if (wps == 0) wps = tc_warps_per_sm(kernel);
+    const int gpw = groups_per_warp(ng, wps);
+    const int64_t warps = (ng + gpw - 1) / gpw;
+    const int64_t blocks = (warps * 32 + 127) / 128;
+    kernel<<<(unsigned)blocks, 128, 0, s>>>(sv, w, n, alpha, grid, gpw);
+  };
+  if (pow2(n))
+    launch(k_spread_cheb<TAB, true, kD>);
+  else
+    launch(k_spread_cheb<TAB, false, kD>);
+}
+
+// AFS_CHEB_SPREAD=0 selects the window-matrix DMMA spread (k_spread_tc) for one right-hand side
+bool cheb_spread_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("AFS_CHEB_SPREAD");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int RG, int TAB>
 void spread_tc(const SortedSide& sv, const Window& w, int n, const double* alpha, int64_t lda,
                int nr, double* grid, int64_t rs, cudaStream_t s) {
+  if (RG == 1 && nr == 1 && cheb_spread_enabled()) return spread_cheb<TAB>(sv, w, n, alpha, grid, s);
   const int64_t ng = sv.ngroups;
   auto launch = [&](auto kernel) {
     static int wps = 0;

@@ -33,6 +33,9 @@
 #ifndef AFS_TC_MINB_CHEB
 #define AFS_TC_MINB_CHEB 4
 #endif
+#ifndef AFS_TC_MINB_CHEB_SPREAD
+#define AFS_TC_MINB_CHEB_SPREAD 3
+#endif
 
 #include "geometry.cuh"
 #include "sliding.cuh"
@@ -693,6 +696,165 @@ __global__ void __launch_bounds__(128, RG == 1 ? AFS_TC_MINB_SPREAD : 1) k_sprea
       for (int r = 0; r < RG; ++r) {
         dmma884(acc[u][r], fx[u][0] * al[u][r][0], fy[u][0]);
         dmma884(acc[u][r], fx[u][1] * al[u][r][1], fy[u][1]);
+      }
+    }
+    st = st1;
+  }
+  cp_async_wait<0>();
+  if (cur_h != -1) flush();
+}
+
+// ----------------------------------------------------------------------------
+// spread, one right-hand side, Chebyshev moments (k_spread_cheb).
+//
+// With phi_a(x) = sum_k Cc[a][k] T_k(4x) (kb_cheb.inc), a half-cell's grid window is
+//     G[a][b] = sum_{k,l} Cc[a][k] M[k][l] Cc[b][l],   M[k][l] = sum_node alpha T_k(4x) T_l(4y)
+// so per group of 8 nodes the tensor cores accumulate the moment matrix M = (alpha T_x)^T T_y
+// (12 x 12) instead of evaluating both window matrices and the touch (8 DMMAs in
+// k_spread_tc).  The block k >= 8, l >= 8 of M (terms below 1e-19 of the window scale) is
+// dropped: 6 DMMAs per group.  The Chebyshev vectors are computed once per node (lane =
+// node) and staged transposed in shared memory for the fragments; the flush folds M back into
+// the 8x8 window with 10 DMMAs per half-cell and warp and adds it to the grid as before.
+// ----------------------------------------------------------------------------
+constexpr int kChebStride = 36;   // staged row length (32 nodes + pad, = 4 mod 16: conflict-free)
+
+template <int TAB, bool POW2, int D>
+__global__ void __launch_bounds__(128, AFS_TC_MINB_CHEB_SPREAD) k_spread_cheb(
+    const SortedSide sv, const Window w, int n, const double* __restrict__ alpha,
+    double* __restrict__ grid, int gpw) {
+  constexpr int U = 4;
+  static_assert(D >= 4, "values are staged two batches ahead of node data landing");
+  __shared__ TcRing<U, D, 1> ring[4];
+  __shared__ __align__(16) double chx[4][12][kChebStride];   // alpha T_k(u) [k][node]
+  __shared__ __align__(16) double chy[4][12][kChebStride];   // T_l(v) [l][node]
+  const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
+  const int wib = threadIdx.x >> 5;
+  TcRing<U, D, 1>& R = ring[wib];
+  double(*CX)[kChebStride] = chx[wib];
+  double(*CY)[kChebStride] = chy[wib];
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g0 = warp * gpw;
+  if (g0 >= sv.ngroups) return;   // warp-uniform
+  const int g1 = min(g0 + gpw, (int)sv.ngroups);
+  double* g = grid + w.grid_off;
+  // flush constants: ck[nb][e] = Cc[slot][2q + e + 8 nb] (step 1: A of N^T = Cc M^T;
+  // step 2: B of G^T = N^T Cc^T, the same values)
+  double ck[2][2];
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = 2 * q + e + 8 * nb;
+      const double c = k < 12 ? kb_cheb<TAB>(slot, k) : 0.0;
+      asm volatile("mov.b64 %0, %1;" : "=d"(ck[nb][e]) : "d"(c));
+    }
+
+  // per-group moment accumulators, block bi in {(0,0), (0,1), (1,0)} of (k-block, l-block):
+  // lane holds M[k = slot + 8 mb][l = 2q + e + 8 nb]
+  double acc[U][3][2];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int bi = 0; bi < 3; ++bi) acc[u][bi][0] = acc[u][bi][1] = 0.0;
+  int32_t cur_h = -1;
+  auto flush = [&]() {
+    double m[3][2];
+#pragma unroll
+    for (int bi = 0; bi < 3; ++bi)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = acc[0][bi][e];
+        acc[0][bi][e] = 0.0;
+#pragma unroll
+        for (int u = 1; u < U; ++u) {
+          v += acc[u][bi][e];
+          acc[u][bi][e] = 0.0;
+        }
+        m[bi][e] = v;
+      }
+    // N^T[b = slot][k = 2q + e' + 8 mb'] = sum_l Cc[b][l] M[k][l], k-steps l = 2q + e + 8 nb
+    double nt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      dmma884(nt[0], ck[0][e], m[0][e]);   // k-block 0, l-block 0
+      dmma884(nt[0], ck[1][e], m[1][e]);   // k-block 0, l-block 1
+      dmma884(nt[1], ck[0][e], m[2][e]);   // k-block 1, l-block 0
+    }
+    // G^T[b = slot][a = 2q + e''] = sum_k N^T[b][k] Cc[a][k], k-steps k = 2q + e' + 8 mb'
+    double gt[2] = {0.0, 0.0};
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dmma884(gt, nt[mb][e], ck[mb][e]);
+    const int col = tc_cell<POW2>(tc_u1(cur_h), tc_c1(cur_h), slot, n);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ix = tc_cell<POW2>(tc_u0(cur_h), tc_c0(cur_h), 2 * q + e, n) * n + col;
+      if (gt[e] != 0.0) grid_add(w, g + ix, gt[e]);
+    }
+  };
+
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    tc_stage_nodes(R, k, sv, g0 + k * U, lane);
+    cp_async_commit();
+  }
+  cp_async_wait<D - 2>();
+  __syncwarp();
+  tc_stage_vals(R, 0, alpha, 0, 1, lane);
+  tc_stage_vals(R, 1, alpha, 0, 1, lane);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  int st = 0;
+#pragma unroll 1
+  for (int gb = g0; gb < g1; gb += U) {
+    cp_async_wait<1>();
+    __syncwarp();   // (also: every lane is done reading the previous batch's vectors)
+    {   // this lane's node: alpha T_k(u) and T_l(v), k, l < 12, into the transposed tables
+      const double u4 = 4.0 * R.x0[st][lane], v4 = 4.0 * R.x1[st][lane];
+      const double a = R.val[st][0][lane];
+      const double u8 = 2.0 * u4, v8 = 2.0 * v4;
+      double tx0 = 1.0, tx1 = u4, ty0 = 1.0, ty1 = v4;
+      CX[0][lane] = a;
+      CY[0][lane] = 1.0;
+      CX[1][lane] = a * u4;
+      CY[1][lane] = v4;
+#pragma unroll
+      for (int k = 2; k < 12; ++k) {
+        const double tx2 = fma(u8, tx1, -tx0), ty2 = fma(v8, ty1, -ty0);
+        CX[k][lane] = a * tx2;
+        CY[k][lane] = ty2;
+        tx0 = tx1;
+        tx1 = tx2;
+        ty0 = ty1;
+        ty1 = ty2;
+      }
+    }
+    int32_t hd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) hd[u] = R.hdr[st][u];
+    const int st1 = st + 1 == D ? 0 : st + 1;
+    const int st2 = st1 + 1 == D ? 0 : st1 + 1;
+    __syncwarp();
+    tc_stage_nodes(R, st, sv, gb + D * U, lane);
+    tc_stage_vals(R, st2, alpha, 0, 1, lane);
+    cp_async_commit();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (hd[u] != cur_h) {   // warp-uniform
+        if (cur_h != -1) flush();
+        cur_h = hd[u];
+      }
+      // M += (alpha T_x)^T T_y over the group's nodes (k-steps: nodes q + 4 s)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int nd = u * 8 + q + 4 * s2;
+        const double a0 = CX[slot][nd], a1 = slot < 4 ? CX[slot + 8][nd] : 0.0;
+        const double b0 = CY[slot][nd], b1 = slot < 4 ? CY[slot + 8][nd] : 0.0;
+        dmma884(acc[u][0], a0, b0);
+        dmma884(acc[u][1], a0, b1);
+        dmma884(acc[u][2], a1, b0);
       }
     }
     st = st1;
