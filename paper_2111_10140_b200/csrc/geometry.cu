@@ -92,7 +92,7 @@ void BuildScratch::reserve_counts(int64_t n) {
   cudaFree(counts); cudaFree(starts);
   counts = nullptr; starts = nullptr; counts_cap = 0;
   AFS_CUDA(cudaMalloc(&counts, sizeof(int32_t) * n));
-  AFS_CUDA(cudaMalloc(&starts, sizeof(int64_t) * 2 * n));
+  AFS_CUDA(cudaMalloc(&starts, sizeof(int64_t) * (2 * n + 2)));   // + 2 totals
   counts_cap = n;
 }
 
@@ -263,6 +263,29 @@ bool tc_eligible(int d, int m, int tab, int n, int64_t N) {
   return !(e && e[0] == '0');
 }
 
+// counts (int32) -> int64 counts and counts rounded up to groups of 8, in place for the scans;
+// the last elements are saved for the totals
+__global__ void k_widen_counts(const int32_t* __restrict__ counts, int64_t nseg,
+                               int64_t* __restrict__ c64, int64_t* __restrict__ p64,
+                               int64_t* __restrict__ last) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nseg) return;
+  const int64_t c = counts[k];
+  c64[k] = c;
+  p64[k] = (c + 7) & ~7LL;
+  if (k == nseg - 1) {
+    last[0] = c;
+    last[1] = (c + 7) & ~7LL;
+  }
+}
+
+// totals = last exclusive-scan entry + last element (written over the saved last elements)
+__global__ void k_scan_totals(const int64_t* __restrict__ seg, const int64_t* __restrict__ pad,
+                              int64_t nseg, int64_t* __restrict__ tot) {
+  tot[0] = seg[nseg - 1] + tot[0];
+  tot[1] = pad[nseg - 1] + tot[1];
+}
+
 void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
                           BuildScratch& sc) {
   if (N >= (int64_t)INT32_MAX / 2) throw Error(AFS_ERR_VALIDATION, "at most 2^30-1 nodes per plan");
@@ -292,19 +315,25 @@ void build_sorted_side_tc(afs_plan* p, const Window& w, const double* X, int64_t
     k_segment_counts<<<bl, th, 0, s>>>(sc.key_b, N, counts);
     AFS_CUDA(cudaGetLastError());
   }
-  std::vector<int32_t> hc(nseg);
-  AFS_CUDA(cudaMemcpy(hc.data(), counts, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost));
-  std::vector<int64_t> hs(2 * nseg);   // [seg_start | pad_start]
-  int64_t pos = 0, pad = 0;
-  for (int64_t k = 0; k < nseg; ++k) {
-    hs[k] = pos;
-    hs[nseg + k] = pad;
-    pos += hc[k];
-    pad += (hc[k] + 7) & ~7;
+  // half-cell starts on the device: seg_start = exclusive scan of the counts, pad_start =
+  // exclusive scan of the counts rounded up to groups of 8 (4 n^2 half-cells: 16.7M at n = 2048)
+  {
+    const int64_t sb = (nseg + th - 1) / th;
+    k_widen_counts<<<(unsigned)sb, th, 0, s>>>(counts, nseg, starts, starts + nseg, starts + 2 * nseg);
+    AFS_CUDA(cudaGetLastError());
+    size_t temp_bytes = 0;
+    AFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, starts, starts, (int)nseg, s));
+    void* temp = sc.sort_temp(temp_bytes);
+    AFS_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, starts, starts, (int)nseg, s));
+    AFS_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, starts + nseg, starts + nseg, (int)nseg, s));
+    k_scan_totals<<<1, 1, 0, s>>>(starts, starts + nseg, nseg, starts + 2 * nseg);
+    AFS_CUDA(cudaGetLastError());
   }
+  int64_t totals[2] = {0, 0};
+  AFS_CUDA(cudaMemcpy(totals, starts + 2 * nseg, sizeof(totals), cudaMemcpyDeviceToHost));
+  const int64_t pad = totals[1];
   const int64_t ngroups = pad / 8;
   const int64_t Npad = pad + 8 * kTcTailGroups;   // trailing empty groups (tc2d.cuh)
-  AFS_CUDA(cudaMemcpy(starts, hs.data(), sizeof(int64_t) * 2 * nseg, cudaMemcpyHostToDevice));
   AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 2 * Npad));
   AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * Npad));
   AFS_CUDA(cudaMalloc(&out->ghdr, sizeof(int32_t) * (Npad / 8)));

@@ -169,7 +169,7 @@ class _Plan:
     """Owns one native plan (afs_plan*) and its staging buffers."""
 
     def __init__(self, X, Z, feats, weights, kernel, config, profile, device, max_rhs,
-                 window_eval="poly", scaling=None, multipliers=None):
+                 window_eval="poly", scaling=None, multipliers=None, coeff_fft="host"):
         torch = _torch()
         self.lib = _native.load()
         self.device = torch.device("cuda", device if device is not None else torch.cuda.current_device())
@@ -212,7 +212,8 @@ class _Plan:
                 coeffs = None
                 mult = np.ascontiguousarray(multipliers[l], dtype=np.float64)
             else:
-                coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w))
+                with torch.cuda.device(self.device):
+                    coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w), coeff_fft)
                 mult = window_multiplier(coeffs, M, n, m)
                 self.windows.append(WindowOperator(w, kernel, config, profile, center, scale,
                                                    coeffs, self.N, self.Nt))
@@ -455,12 +456,14 @@ class AnovaKernelOperator:
     ``windows`` follows the reference (a ``WindowSet`` or a list validated as
     one).  ``strict=False`` accepts arbitrary, possibly overlapping windows
     (the C3/C5 recipes); ``weights`` overrides eta_l = 1/P in that mode.
-    ``max_rhs`` sizes the workspace for multi-column alpha.
+    ``max_rhs`` sizes the workspace for multi-column alpha.  ``coeff_fft="device"``
+    computes c_hat's plan-time transform with cuFFT instead of scipy's pocketfft
+    (spectrum.regularize_kernel).
     """
 
     def __init__(self, X, windows, sigma, profile="default", targets=None, config=None, *,
                  strict=True, weights=None, device=None, max_rhs=1, window_eval="poly",
-                 scaling=None, deterministic=False):
+                 scaling=None, deterministic=False, coeff_fft="host"):
         X = _as_matrix(X, "sources")
         if strict:
             if not isinstance(windows, WindowSet):
@@ -489,7 +492,7 @@ class AnovaKernelOperator:
         self.n_sources = X.shape[0]
         self.n_targets = X.shape[0] if Z is None else Z.shape[0]
         self._plan = _Plan(X, Z, list(windows.windows), list(windows.weights), kernel, config,
-                           profile, device, max_rhs, window_eval, scaling)
+                           profile, device, max_rhs, window_eval, scaling, coeff_fft=coeff_fft)
         if deterministic:
             self._plan.set_deterministic(True)
         self.operators = self._plan.windows
@@ -515,7 +518,7 @@ class FastsumOperator:
     """
 
     def __init__(self, kernel, config, sources, targets=None, profile="default", *, device=None,
-                 max_rhs=1, window_eval="poly", deterministic=False):
+                 max_rhs=1, window_eval="poly", deterministic=False, coeff_fft="host"):
         if not isinstance(kernel, GaussianKernel):
             raise ValidationError("kernel must be a GaussianKernel")
         profile = resolve_profile(profile)
@@ -535,7 +538,7 @@ class FastsumOperator:
         self.profile = profile
         self.dims = d
         self._plan = _Plan(X, Z, [tuple(range(d))], [1.0], kernel, config, profile, device, max_rhs,
-                           window_eval)
+                           window_eval, coeff_fft=coeff_fft)
         self._nodes = (X, Z)             # for the lazily built NfftPlan views
         self._nfft = {}
         self._device = device

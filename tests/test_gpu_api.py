@@ -104,3 +104,29 @@ def test_concurrent_applies_match_serial(afs, deterministic):
             np.testing.assert_array_equal(results[k], serial[k])
         else:
             assert rel_l2(results[k], serial[k]) < 1e-14
+
+
+@pytest.mark.parametrize("sigma,M,d", [(0.05, 32, 2), (0.3, 16, 3), (0.1, 128, 3)])
+def test_device_coefficient_fft_matches_pocketfft(afs, sigma, M, d):
+    """c_hat with the plan-time transform on cuFFT (coeff_fft="device", row f2) against the
+    reference-identical pocketfft path: roundoff-level agreement."""
+    from paper_2111_10140_b200.spectrum import regularize_kernel
+
+    cfg = afs.PeriodizationConfig(coeff_grid=M)
+    host = regularize_kernel(afs.GaussianKernel(sigma), cfg, d)
+    dev = regularize_kernel(afs.GaussianKernel(sigma), cfg, d, fft="device")
+    err = rel_l2(dev, host)
+    print(f"c_hat sigma={sigma} M={M} d={d}: device vs pocketfft rel l2 {err:.2e}")
+    assert err < 1e-14
+
+
+def test_device_coefficient_fft_operator_matches_reference(afs, golden):
+    from paper_2111_10140_b200 import synthetic
+
+    w = synthetic.c3(N=1500)
+    op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("b", 2.0, w.m), None,
+                                 afs.PeriodizationConfig(coeff_grid=w.M), strict=False,
+                                 coeff_fft="device")
+    err = rel_l2(op.apply(w.alpha), golden["c3s_out"])
+    print(f"C3s with device c_hat: rel l2 {err:.2e}")
+    assert err < 1e-10
