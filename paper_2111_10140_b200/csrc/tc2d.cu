@@ -42,6 +42,22 @@ int groups_per_warp(int64_t ngroups, int warps_per_sm) {
 
 bool pow2(int n) { return (n & (n - 1)) == 0; }
 
+// The Chebyshev kernels fold a whole half-cell once per warp (10 DMMAs); they pay when a
+// half-cell holds several groups (C3: ~19 groups per half-cell, gather -7%, spread -7%) and
+// lose at low density (C5 pairs at N = 1M, ~2.4 groups: spread +17%).  AFS_CHEB=0/1 forces
+// the gather choice, AFS_CHEB_SPREAD=0/1 the spread's (A/B hooks); default: by density.
+constexpr double kChebMinGroupsPerHalfCell = 8.0;
+
+int env_switch(const char* name) {   // -1 unset, else 0/1
+  const char* e = getenv(name);
+  return e ? (e[0] == '0' ? 0 : 1) : -1;
+}
+
+bool dense_enough(const SortedSide& sv, int n) {
+  return (double)sv.ngroups >= kChebMinGroupsPerHalfCell * 4.0 * (double)n * (double)n;
+}
+
+
 template <int TAB>
 void spread_cheb(const SortedSide& sv, const Window& w, int n, const double* alpha, double* grid,
                  cudaStream_t s) {
@@ -60,20 +76,15 @@ void spread_cheb(const SortedSide& sv, const Window& w, int n, const double* alp
     launch(k_spread_cheb<TAB, false, kD>);
 }
 
-// AFS_CHEB_SPREAD=0 selects the window-matrix DMMA spread (k_spread_tc) for one right-hand side
-bool cheb_spread_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("AFS_CHEB_SPREAD");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
+bool cheb_spread_enabled(const SortedSide& sv, int n) {
+  static const int force = env_switch("AFS_CHEB_SPREAD");
+  return force >= 0 ? force == 1 : dense_enough(sv, n);
 }
 
 template <int RG, int TAB>
 void spread_tc(const SortedSide& sv, const Window& w, int n, const double* alpha, int64_t lda,
                int nr, double* grid, int64_t rs, cudaStream_t s) {
-  if (RG == 1 && nr == 1 && cheb_spread_enabled()) return spread_cheb<TAB>(sv, w, n, alpha, grid, s);
+  if (RG == 1 && nr == 1 && cheb_spread_enabled(sv, n)) return spread_cheb<TAB>(sv, w, n, alpha, grid, s);
   const int64_t ng = sv.ngroups;
   auto launch = [&](auto kernel) {
     static int wps = 0;
@@ -89,14 +100,9 @@ void spread_tc(const SortedSide& sv, const Window& w, int n, const double* alpha
     launch(k_spread_tc<RG, TAB, kU, false, kD>);
 }
 
-// AFS_CHEB=0 selects the DMMA gather (k_gather_tc) for one right-hand side too (A/B hook)
-bool cheb_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("AFS_CHEB");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
+bool cheb_enabled(const SortedSide& sv, int n) {
+  static const int force = env_switch("AFS_CHEB");
+  return force >= 0 ? force == 1 : dense_enough(sv, n);
 }
 
 template <int TAB>
@@ -120,7 +126,7 @@ void gather_cheb(const SortedSide& sv, const Window& w, int n, const double* gri
 template <int RG, int TAB>
 void gather_tc(const SortedSide& sv, const Window& w, int n, const double* grid, int64_t rs, int nr,
                double* out, int64_t ldo, cudaStream_t s) {
-  if (RG == 1 && nr == 1 && cheb_enabled()) return gather_cheb<TAB>(sv, w, n, grid, out, s);
+  if (RG == 1 && nr == 1 && cheb_enabled(sv, n)) return gather_cheb<TAB>(sv, w, n, grid, out, s);
   const int64_t ng = sv.ngroups;
   auto launch = [&](auto kernel) {
     static int wps = 0;

@@ -162,7 +162,9 @@ def job_c5cg():
 def job_c2pert(k):
     """The reference's own roundoff sensitivity on the named C2 solve: the same recipe with
     the three windows summed in another order (FastsumOperators composed as
-    AnovaKernelOperator.apply does, anova.py:179-183), CG at 50 and 200 iterations."""
+    AnovaKernelOperator.apply does, anova.py:179-183), CG at 50 and 200 iterations.
+    With three windows only two orders change the rounding ((c+b)+a and (a+c)+b; k = 0, 2):
+    k = 1 ((b+a)+c) reproduces the golden bit for bit and is not kept."""
     order = [[2, 1, 0], [1, 0, 2], [0, 2, 1]][k]
     w = synthetic.c2()
     prof = AccuracyProfile("default", 2.0, 4)
