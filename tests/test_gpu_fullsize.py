@@ -189,7 +189,15 @@ def test_c2_full_size_cg_matches_reference(afs, deterministic):
               f"{rel_l2(gold['x'], tight.x):.3e} (tight: {tight.iterations} it)")
         assert abs(res.iterations - int(gold["iters"])) <= max(1, its + 1)
         assert err < max(CG_TOL, 4 * xs)
+    # decision values: the same bar in decision space -- the reference's reordered solutions
+    # pushed through the (parity-checked) GPU predict operator give its own spread there
+    import glob
+
     pred = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, "default", targets=w.Z)
+    d_ref = pred.apply(g["x"])
+    assert rel_l2(d_ref, g["decision"]) < 1e-10
+    ds = max(rel_l2(pred.apply(np.load(p)["x200"]), d_ref)
+             for p in sorted(glob.glob(os.path.join(HERE, "golden", "golden_c2pert*.npz"))))
     err_d = rel_l2(pred.apply(res.x), g["decision"])
-    print(f"C2 decision values [{mode}]: rel l2 {err_d:.3e}")
-    assert err_d < max(CG_TOL, 4 * xs)
+    print(f"C2 decision values [{mode}]: rel l2 {err_d:.3e}; reference self-spread {ds:.3e}")
+    assert err_d < max(CG_TOL, 4 * ds)
