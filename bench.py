@@ -63,6 +63,8 @@ def parse(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--deterministic", action="store_true",
                     help="bit-reproducible fixed-point spread (afs_plan_set_deterministic)")
+    if argv is None and os.environ.get("AFS_BENCH_ARGV"):
+        argv = json.loads(os.environ["AFS_BENCH_ARGV"])   # set by relaunch_under_torchrun
     a = ap.parse_args(argv)
     if a.n is None:
         a.n = FULL_N[a.config]
@@ -77,8 +79,11 @@ def relaunch_under_torchrun(args):
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
-           os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+           os.path.abspath(__file__)]
+    # the ranks get this command line through the environment: torchrun's own argument parser
+    # would otherwise see (and reject as ambiguous) options such as --n after the script
+    env = dict(os.environ, AFS_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    return subprocess.call(cmd, env=env)
 
 
 def algorithmic_bytes(N, windows, n, R=1):
