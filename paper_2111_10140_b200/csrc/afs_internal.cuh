@@ -129,6 +129,13 @@ struct afs_plan {
   cudaEvent_t ev_join[kMaxBranches - 1] = {nullptr, nullptr, nullptr};
   int stage_streams = 0;            // 0: automatic (branch_count), else fixed 1..4
   double* outx[kMaxBranches - 1] = {nullptr, nullptr, nullptr};   // [max_rhs][Nt] each
+  // window pipeline (apply_pipeline, pipeline.cu): spread streams and gather streams apart, so
+  // a window's gather starts when its own spread + spectral are done
+  cudaStream_t pipe_s[kMaxBranches] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t pipe_g[kMaxBranches - 1] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_fork = nullptr;
+  cudaEvent_t pipe_join[2 * kMaxBranches - 1] = {};
+  std::vector<cudaEvent_t> unit_ev;   // one per pipeline unit
   bool profiling = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double stage_ms[3] = {0.0, 0.0, 0.0};
@@ -156,6 +163,16 @@ void spectral_all(afs_plan* p, int R, cudaStream_t s, int mode = 0);   // 0 fuse
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
 void apply_impl(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
                 int R, cudaStream_t s);
+// per-unit stages of the window pipeline (a unit = one window, or all batched 1-D windows)
+void spread_unit(afs_plan* p, const std::vector<int>& wins, bool batch1d, const double* alpha,
+                 int64_t lda, int R, cudaStream_t s);
+void spectral_windows(afs_plan* p, int R, cudaStream_t s, const std::vector<int>& wins);
+void gather_unit(afs_plan* p, const std::vector<int>& wins, bool fused1d, double* out,
+                 int64_t ldo, int R, cudaStream_t s);
+bool gather_1d_fusable(const afs_plan* p);
+bool pipeline_applies(const afs_plan* p);
+void apply_pipeline(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
+                    int R, cudaStream_t s);
 // the three stages on stream s, no graph (capturable once a warm-up apply ran: allocations
 // and one-time kernel attributes happen on first use)
 void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,

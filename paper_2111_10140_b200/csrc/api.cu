@@ -51,6 +51,10 @@ void make_twiddles(afs_plan* p) {
 
 void apply_stages(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
                   int R, cudaStream_t s) {
+  if (pipeline_applies(p)) {   // per-window pipeline (pipeline.cu)
+    apply_pipeline(p, alpha, lda, out, ldo, R, s);
+    return;
+  }
   spread_all(p, alpha, lda, R, s);
   spectral_all(p, R, s);
   gather_all(p, out, ldo, R, s);
@@ -203,6 +207,14 @@ static void free_plan(afs_plan* p) {
     cudaFree(p->outx[b]);
   }
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  for (cudaStream_t st : p->pipe_s)
+    if (st) cudaStreamDestroy(st);
+  for (cudaStream_t st : p->pipe_g)
+    if (st) cudaStreamDestroy(st);
+  if (p->pipe_fork) cudaEventDestroy(p->pipe_fork);
+  for (cudaEvent_t e : p->pipe_join)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->unit_ev) cudaEventDestroy(e);
   if (p->cg.host_scalars) cudaFreeHost(p->cg.host_scalars);
   if (!p->parent) {
     for (SortedSide* s : p->src_side)

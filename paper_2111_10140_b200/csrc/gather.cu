@@ -163,8 +163,17 @@ int gather_branches(const afs_plan* p, int R) {
   return nb;
 }
 
-bool gather_1d_fusable(const afs_plan* p);
 void gather_1d_fused(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s);
+
+void gather_unit(afs_plan* p, const std::vector<int>& wins, bool fused1d, double* out,
+                 int64_t ldo, int R, cudaStream_t s) {
+  if (fused1d) {   // every 1-D window of the plan, in window order, in shared launches
+    gather_1d_fused(p, out, ldo, R, s);
+    return;
+  }
+  for (int l : wins)
+    if (!gather_v2_window(p, l, out, ldo, R, s)) gather_v1(p, l, l + 1, out, ldo, R, s);
+}
 
 void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
   // out = 0, then out += eta_l * s_l in window order (anova.py:179-183)

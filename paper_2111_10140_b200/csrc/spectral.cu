@@ -626,14 +626,32 @@ static void run_pass(afs_plan* pl, LinePass p, const BatchOff& off, int nb, cuda
 // in pl->spec (layout of the multiplier, complex).  mode 2: pruned spectrum -> grid.
 // Modes 1 + 2 split the stage so point-sharded ranks can all-reduce the spectrum (linear in
 // the nodes) instead of the oversampled grid: K^(d-1)*(M/2+1) instead of n^d values.
+static void spectral_subset(afs_plan* pl, int R, cudaStream_t s, int mode,
+                            const std::vector<int>* only);
+
 void spectral_all(afs_plan* pl, int R, cudaStream_t s, int mode) {
+  spectral_subset(pl, R, s, mode, nullptr);
+}
+
+// the fused stage (mode 0) for a subset of the windows (the window pipeline's units)
+void spectral_windows(afs_plan* pl, int R, cudaStream_t s, const std::vector<int>& wins) {
+  spectral_subset(pl, R, s, 0, &wins);
+}
+
+static void spectral_subset(afs_plan* pl, int R, cudaStream_t s, int mode,
+                            const std::vector<int>* only) {
   const int n = pl->n, M = pl->M, H = pl->H, K = M + 1;
   const int64_t gs = pl->grid_total;
   const int64_t ss = pl->spec_total;
   for (int d = 1; d <= 3; ++d) {
     std::vector<int> ws;
-    for (int l = 0; l < pl->P; ++l)
-      if (pl->win[l].d == d) ws.push_back(l);
+    if (only) {
+      for (int l : *only)
+        if (pl->win[l].d == d) ws.push_back(l);
+    } else {
+      for (int l = 0; l < pl->P; ++l)
+        if (pl->win[l].d == d) ws.push_back(l);
+    }
     for (size_t b0 = 0; b0 < ws.size(); b0 += kMaxBatch) {
       const int nb = (int)std::min<size_t>(kMaxBatch, ws.size() - b0);
       BatchOff grid_off{}, a_off{}, b_off{}, m_off{}, s_off{};

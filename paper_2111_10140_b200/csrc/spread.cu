@@ -287,4 +287,35 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   AFS_CUDA(cudaGetLastError());
 }
 
+void spread_unit(afs_plan* p, const std::vector<int>& wins, bool batch1d, const double* alpha,
+                 int64_t lda, int R, cudaStream_t s) {
+  if (batch1d) {   // the 1-D windows' solo spreads in shared launches (grids disjoint)
+    for (size_t b0 = 0; b0 < wins.size(); b0 += kSoloBatch) {
+      SoloBatch B{};
+      B.nwin = (int)std::min<size_t>(kSoloBatch, wins.size() - b0);
+      for (int i = 0; i < B.nwin; ++i) {
+        B.sv[i] = *p->src_side[wins[b0 + i]];
+        B.w[i] = p->win[wins[b0 + i]];
+      }
+      launch_spread_solo_batch_1d(B, p->n, p->m, p->kb_tab, *p->poly, alpha, lda, R, p->grids,
+                                  p->grid_total, s);
+    }
+    return;
+  }
+  for (int l : wins) {
+    if (spread_v2_window(p, l, alpha, lda, R, s)) continue;
+    const Window& w = p->win[l];
+    switch (p->m) {
+      case 1: launch_spread_m<1>(p, w, alpha, lda, R, s); break;
+      case 2: launch_spread_m<2>(p, w, alpha, lda, R, s); break;
+      case 3: launch_spread_m<3>(p, w, alpha, lda, R, s); break;
+      case 4: launch_spread_m<4>(p, w, alpha, lda, R, s); break;
+      case 5: launch_spread_m<5>(p, w, alpha, lda, R, s); break;
+      case 6: launch_spread_m<6>(p, w, alpha, lda, R, s); break;
+      case 7: launch_spread_m<7>(p, w, alpha, lda, R, s); break;
+      default: launch_spread_m<8>(p, w, alpha, lda, R, s); break;
+    }
+  }
+}
+
 }  // namespace afs
