@@ -7,6 +7,7 @@
 #include "afs_internal.cuh"
 
 #include <cstdlib>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx (no-ops untraced)
 #include "geometry.cuh"
 
 namespace afs {
@@ -475,7 +476,15 @@ int afs_abi_version(void) { return AFS_ABI_VERSION; }
 
 const char* afs_last_error(void) { return afs::g_last_error.c_str(); }
 
+namespace {
+struct NvtxRange {   // scoped NVTX range around one C-ABI call
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 int afs_plan_create(const afs_plan_desc* desc, afs_plan** plan) {
+  NvtxRange r("afs_plan_create");
   return afs::guarded([&] { afs::create_plan(desc, plan); });
 }
 
@@ -673,6 +682,7 @@ int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, 
 
 int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out, int64_t ld_out,
               int32_t nrhs, void* stream) {
+  NvtxRange r("afs_apply");
   return afs::guarded([&] {
     if (!plan) throw afs::Error(AFS_ERR_VALIDATION, "null plan");
     if (nrhs < 1 || nrhs > plan->max_rhs)
@@ -752,6 +762,7 @@ int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out
 int afs_cg_solve(afs_plan* plan, const double* b, double* x, double beta, double tol,
                  int32_t maxiter, int32_t* iterations, double* residual, int32_t* converged,
                  void* stream) {
+  NvtxRange r("afs_cg_solve");
   int it = 0, conv = 0;
   double res = 0.0;
   const int st = afs::guarded([&] {

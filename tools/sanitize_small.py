@@ -1,8 +1,10 @@
 """Small end-to-end run of every kernel family for compute-sanitizer (memcheck/racecheck):
 
     compute-sanitizer --tool memcheck python tools/sanitize_small.py
-covers 1-D/2-D/3-D windows, the tensor-core 2-D and (AFS_TC3=1) 3-D kernels, targets,
-multi-RHS, deterministic mode and the device CG."""
+covers 1-D/2-D/3-D windows, the tensor-core 2-D kernels (window-matrix and, forced on here,
+Chebyshev), the (AFS_TC3=1) 3-D tensor-core kernels, targets, multi-RHS, the per-window
+pipeline, deterministic mode, the device CG (whole-solve graph, fused cooperative epilogue),
+concurrent applies on workspace clones, apply_complex and the sharded-CG vector kernels."""
 import os
 import sys
 
@@ -13,6 +15,8 @@ import numpy as np  # noqa: E402
 import paper_2111_10140_b200 as afs  # noqa: E402
 
 os.environ.setdefault("AFS_TC3", "1")
+os.environ.setdefault("AFS_CHEB", "1")
+os.environ.setdefault("AFS_CHEB_SPREAD", "1")
 rng = np.random.default_rng(0)
 N, Nt = 3000, 1000
 centers = rng.uniform(-0.2, 0.2, size=(3, 6))
@@ -31,3 +35,37 @@ det = afs.AnovaKernelOperator(X, windows, 0.3, prof, None, cfg, strict=False, ma
 det.apply(A)
 res = afs.cg_solve(afs.KernelSystem(det, 0.5), A[:, 1], tol=1e-8, maxiter=30)
 print("cg", res.iterations, res.residual)
+
+res = afs.cg_solve(afs.KernelSystem(op_sq := afs.AnovaKernelOperator(X, windows, 0.3, prof, None, cfg,
+                                                                     strict=False), 0.5),
+                   A[:, 2], tol=1e-8, maxiter=30)
+print("cg (atomic, pipeline)", res.iterations, res.residual)
+
+import threading  # noqa: E402
+
+import torch  # noqa: E402
+
+outs = [None] * 4
+
+
+def worker(k):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        outs[k] = op_sq.apply(torch.from_numpy(A[:, k % 3].copy()).cuda()).cpu().numpy()
+
+
+ths = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+for t in ths:
+    t.start()
+for t in ths:
+    t.join()
+print("concurrent applies", float(np.max(np.abs(outs[0] - outs[3]))))
+
+fs = afs.FastsumOperator(afs.GaussianKernel(0.3), cfg, X[:, :2], Z[:, :2], prof)
+print("apply_complex", float(np.abs(fs.apply_complex(A[:, 0] + 1j * A[:, 1])).max()))
+
+from paper_2111_10140_b200.cg import CudaCgVectors, run_cg  # noqa: E402
+
+b = torch.from_numpy(A[:, 0].copy()).cuda()
+r = run_cg(lambda v: op_sq.apply(v), b, 0.5, 1e-8, 20, CudaCgVectors(b.device))
+print("vector-kernel cg", r.iterations, r.residual)
