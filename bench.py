@@ -131,6 +131,23 @@ class ClockSampler:
         self.rows = []
         self.source = None
 
+    def _nvml_handle(self, nv):
+        """NVML handle of CUDA device self.idx, matched by UUID (CUDA and NVML orders can
+        differ, e.g. under CUDA_VISIBLE_DEVICES); the NVML index as a fallback."""
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(self.idx).uuid)
+            for i in range(nv.nvmlDeviceGetCount()):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                u = nv.nvmlDeviceGetUUID(h)
+                u = u.decode() if isinstance(u, bytes) else u
+                if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                    return h
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetHandleByIndex(self.idx)
+
     def _nvml_loop(self, nv, h):
         while not self.stop:
             try:
@@ -152,7 +169,7 @@ class ClockSampler:
             import pynvml as nv
 
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            h = self._nvml_handle(nv)
             self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self.stop = False
             self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)

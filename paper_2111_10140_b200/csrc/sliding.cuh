@@ -29,8 +29,11 @@ namespace afs {
 // 4 blocks (<= 128 registers, no spills at m = 4; C3 3-D windows 4% faster than 3 blocks);
 // two at a time need their registers (capped they spill: C4 gather 6.8 -> 8.9 ms)
 // (m <= 4; larger cutoffs spill under the cap)
+#ifndef AFS_TEAM3_MINB
+#define AFS_TEAM3_MINB 4
+#endif
 template <int D, int MM, int RG>
-constexpr int v2_min_blocks() { return (D == 3 && RG == 1 && MM <= 4) ? 4 : 1; }
+constexpr int v2_min_blocks() { return (D == 3 && RG == 1 && MM <= 4) ? AFS_TEAM3_MINB : 1; }
 #ifndef AFS_TEAM3
 #define AFS_TEAM3 32   // lanes per run for 3-D windows (power of two, 8..32)
 #endif
