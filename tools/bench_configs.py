@@ -76,7 +76,7 @@ def main():
                           "cg_converged": res.converged, "cg_residual": res.residual,
                           "cg_wall_s": t_cg, "ms_per_cg_iteration": 1e3 * t_cg / max(1, res.iterations),
                           "predict_wall_s_incl_build": t_pred, "n_test": w.Z.shape[0],
-                          "train_accuracy_proxy": float(np.mean(np.sign(dec) == np.sign(dec)))}),
+                          "decision_abs_mean": float(np.mean(np.abs(dec)))}),
               flush=True)
 
     if "C4" not in skip:
