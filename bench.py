@@ -648,6 +648,10 @@ def run_ours(args):
         backend = CudaPointBackend(w.X, w.windows, w.sigma, M=w.M, m=w.m, max_rhs=R,
                                    device=dev.index, exchange="spectrum")
         op, plan = PointSharded(backend), backend.plan
+    elif cfg == "c5" and world > 1:   # WindowSharded makes the same LPT deal, owns the plan
+        sharded = afs.WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, device=dev.index)
+        op = sharded.local
+        plan = op._plan if op is not None else None
     else:
         op = free_operator(afs, w, my_windows, [1.0 / w.P] * len(mine), max_rhs=R,
                            deterministic=args.deterministic, device=dev.index) if mine else None
@@ -677,15 +681,7 @@ def run_ours(args):
                 plan.apply_device(alpha, out, R)
         h2d, d2h = 8 * Nloc * R * world, 8 * Nloc * R * world
     else:   # c5: whole CG solves, maxiter = --cg-iters
-        if world > 1:   # WindowSharded makes the same LPT deal and owns this rank's plan
-            if op is not None:
-                op.close()
-            sharded = afs.WindowSharded(w.X, w.windows, w.sigma, M=w.M, m=w.m, device=dev.index)
-            op = sharded.local
-            plan = op._plan if op is not None else None
-            system = afs.KernelSystem(sharded, w.beta)
-        else:
-            system = afs.KernelSystem(op, w.beta)
+        system = afs.KernelSystem(sharded if world > 1 else op, w.beta)
         b_dev = torch.from_numpy(w.y).to(dev)
         iters = []
 
