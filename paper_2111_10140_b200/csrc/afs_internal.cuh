@@ -148,6 +148,7 @@ struct afs_plan {
   // clones -- plans that share this plan's immutable geometry (sorted sides, multipliers,
   // coordinates, tables) and own their grids, scratch, limbs, streams and graphs
   afs_plan* parent = nullptr;            // set on clones: nothing shared is freed with them
+  int64_t mode_gen = 0;                  // bumped when the mode changes; clones record theirs
   std::vector<afs_plan*> clones;
   std::vector<char> clone_busy;
   bool primary_busy = false;

@@ -277,6 +277,7 @@ static afs_plan* make_clone(afs_plan* p) {
     c->stage_streams = p->stage_streams;
     c->det_log2_bound = p->det_log2_bound;
     c->deterministic = p->deterministic;
+    c->mode_gen = p->mode_gen;
     AFS_CUDA(cudaMalloc(&c->grids, sizeof(double) * c->grid_total * c->max_rhs));
     if (c->scratch_a_len)
       AFS_CUDA(cudaMalloc(&c->scratch_a, sizeof(double2) * c->scratch_a_len * c->max_rhs));
@@ -638,7 +639,11 @@ int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
       AFS_CUDA(cudaMalloc(&plan->det_aux, 4 * sizeof(double)));
       plan->device_bytes += (int64_t)bytes + 4 * (int64_t)sizeof(double);
     }
-    plan->deterministic = enable != 0;
+    {
+      std::lock_guard<std::mutex> lk(plan->pool_mu);
+      plan->deterministic = enable != 0;
+      ++plan->mode_gen;   // clones made meanwhile are rebuilt at their next use
+    }
     afs::refresh_det_windows(plan);
   });
 }
@@ -710,6 +715,13 @@ int afs_apply(afs_plan* plan, const double* alpha, int64_t ld_alpha, double* out
         }
         for (slot = 0; slot < plan->clones.size(); ++slot)
           if (!plan->clone_busy[slot]) break;
+        if (slot < plan->clones.size() && plan->clones[slot]->mode_gen != plan->mode_gen) {
+          // made before a mode change (set_deterministic raced with this apply): rebuild
+          afs::free_plan(plan->clones[slot]);
+          plan->clones.erase(plan->clones.begin() + slot);
+          plan->clone_busy.erase(plan->clone_busy.begin() + slot);
+          continue;
+        }
         if (slot < plan->clones.size()) {
           plan->clone_busy[slot] = 1;
           target = plan->clones[slot];
