@@ -94,10 +94,14 @@ class FreeWindowSet:
 
 
 class WindowOperator:
-    """Per-window view with the FastsumOperator attributes (fastsum.py:219-232)."""
+    """One window's term K_l of an ANOVA operator, as the reference's ``operators[l]``
+    (anova.py:163-172): the FastsumOperator attributes (fastsum.py:219-232) are the plan's
+    own; ``apply`` / ``apply_complex`` / ``source_plan`` / ``target_plan`` build a GPU
+    ``FastsumOperator`` on the window's columns at first use (the ANOVA apply itself never
+    needs it: all windows run in one plan)."""
 
     def __init__(self, features, kernel, config, profile, center, scale, coeffs, n_sources,
-                 n_targets):
+                 n_targets, nodes=None, device=None, window_eval="poly"):
         self.features = tuple(features)
         self.kernel = kernel
         self.config = config
@@ -109,6 +113,35 @@ class WindowOperator:
         self.coeffs = coeffs
         self.n_sources = n_sources
         self.n_targets = n_targets
+        self._nodes = nodes              # (X, Z) of the whole operator, or None
+        self._device = device
+        self._window_eval = window_eval
+        self._op = None
+
+    def _fastsum(self):
+        if self._op is None:
+            if self._nodes is None:
+                raise ValidationError("this window view has no nodes to build an operator on")
+            X, Z = self._nodes
+            cols = list(self.features)
+            self._op = FastsumOperator(self.kernel, self.config, X[:, cols],
+                                       None if Z is None else Z[:, cols], self.profile,
+                                       device=self._device, window_eval=self._window_eval)
+        return self._op
+
+    def apply(self, alpha):
+        return self._fastsum().apply(alpha)
+
+    def apply_complex(self, alpha):
+        return self._fastsum().apply_complex(alpha)
+
+    @property
+    def source_plan(self):
+        return self._fastsum().source_plan
+
+    @property
+    def target_plan(self):
+        return self._fastsum().target_plan
 
 
 def bbox_scaling(lo, hi, config):
@@ -216,7 +249,9 @@ class _Plan:
                     coeffs = regularize_kernel(kernel.rescaled(scale), config, len(w), coeff_fft)
                 mult = window_multiplier(coeffs, M, n, m)
                 self.windows.append(WindowOperator(w, kernel, config, profile, center, scale,
-                                                   coeffs, self.N, self.Nt))
+                                                   coeffs, self.N, self.Nt, nodes=(X, Z),
+                                                   device=self.device.index,
+                                                   window_eval=window_eval))
             self._keep.append(mult)
             dsc = descs[l]
             dsc.dims = len(w)

@@ -130,3 +130,25 @@ def test_device_coefficient_fft_operator_matches_reference(afs, golden):
     err = rel_l2(op.apply(w.alpha), golden["c3s_out"])
     print(f"C3s with device c_hat: rel l2 {err:.2e}")
     assert err < 1e-10
+
+
+def test_anova_operators_are_per_window_fastsum_operators(afs):
+    """operators[l] of an ANOVA operator behaves like the reference's FastsumOperator on the
+    window's columns (anova.py:163-172): same scaling, and apply equals the oracle's
+    single-window fast sum; the weighted sum of the terms equals the ANOVA apply."""
+    from oracle import fastsum_oracle as orc
+    from paper_2111_10140_b200 import synthetic
+
+    w = synthetic.c1(N=2000)
+    Z = np.random.default_rng(2).standard_normal((500, 9))
+    op = afs.AnovaKernelOperator(w.X, w.windows, w.sigma, afs.AccuracyProfile("c1", 2.0, 2),
+                                 targets=Z, config=afs.PeriodizationConfig(coeff_grid=32))
+    total = np.zeros(500)
+    for eta, win, term in zip(op.windows.weights, w.windows, op.operators):
+        got = term.apply(w.alpha)
+        ref = orc.fastsum_apply(w.X[:, list(win)], w.alpha, w.sigma, 32, 2, 2.0,
+                                Z=Z[:, list(win)])
+        assert rel_l2(got, ref) < 1e-10
+        assert term.source_plan.node_count == 2000 and term.target_plan.node_count == 500
+        total += eta * got
+    assert rel_l2(op.apply(w.alpha), total) < 1e-14
