@@ -12,7 +12,8 @@ KEYS = ["gpu__time_duration.sum", "sm__pipe_shared_cycles_active.avg.pct_of_peak
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "launch__registers_per_thread",
         "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
         "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sectors_op_red.sum", "sm__inst_executed_pipe_fp64.sum"]
 
 
 def main(name):
