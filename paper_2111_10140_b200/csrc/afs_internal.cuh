@@ -171,6 +171,11 @@ void spectral_windows(afs_plan* p, int R, cudaStream_t s, const std::vector<int>
 void gather_unit(afs_plan* p, const std::vector<int>& wins, bool fused1d, double* out,
                  int64_t ldo, int R, cudaStream_t s);
 bool gather_1d_fusable(const afs_plan* p);
+void det_prepare(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s);
+void clear_rows(void* base, int64_t arr_stride, int narr, int64_t pitch, int64_t width, int R,
+                cudaStream_t s);
+void det_window_begin(afs_plan* p, const Window& w, int R, cudaStream_t s);
+void det_window_finalize(afs_plan* p, const Window& w, int R, cudaStream_t s);
 bool pipeline_applies(const afs_plan* p);
 void apply_pipeline(afs_plan* p, const double* alpha, int64_t lda, double* out, int64_t ldo,
                     int R, cudaStream_t s);

@@ -9,7 +9,9 @@
 // do, so results are run-to-run reproducible.  Plans with few windows gain (C2: three 3-D
 // windows at N = 100k, 0.226 -> 0.203 ms per matvec): the stage barriers and per-stage tails
 // were a large part of their apply.  Deterministic mode, profiling and plans with more than
-// 8 windows keep the staged path (apply_stages); AFS_PIPELINE=0/1 forces the choice.
+// 8 windows keep the staged path (apply_stages); AFS_PIPELINE=0/1 forces the choice.  In
+// deterministic mode the scale 2^S is set once per apply before the fork and every window
+// clears its own limbs before its spread and converts them after it.
 #include <algorithm>
 #include <cstdlib>
 
@@ -28,8 +30,9 @@ bool pipeline_applies(const afs_plan* p) {
     return e ? (e[0] == '0' ? 0 : 1) : -1;
   }();
   if (force == 0) return false;
-  if (p->window_eval != 0 || p->deterministic || p->profiling || p->P < 2) return false;
-  // measured: C2 (3 windows) -10% per matvec; C5 (30 windows) +4%, C3 (39) +-0 -- with many
+  if (p->window_eval != 0 || p->profiling || p->P < 2) return false;
+  // measured: C2 (3 windows) -10% per matvec (deterministic CG: 0.367 -> 0.344 ms per iteration);
+  // C5 (30 windows) +4%, C3 (39) +-0 -- with many
   // windows the staged branches already overlap the tails, and the per-window spectral
   // launches cost more than the barriers they remove
   if (force < 0 && p->P > 8) return false;
@@ -93,6 +96,8 @@ void apply_pipeline(afs_plan* p, const double* alpha, int64_t lda, double* out, 
       p->device_bytes += sizeof(double) * p->Nt * p->max_rhs;
     }
 
+  const bool det = p->deterministic && p->det_limbs;
+  if (det) det_prepare(p, alpha, lda, R, s);   // 2^S from max|alpha|, before the fork
   // fork: every stream starts after the caller's work (alpha, out)
   AFS_CUDA(cudaEventRecord(p->pipe_fork, s));
   for (int b = 0; b < ns; ++b) AFS_CUDA(cudaStreamWaitEvent(p->pipe_s[b], p->pipe_fork, 0));
@@ -106,10 +111,15 @@ void apply_pipeline(afs_plan* p, const double* alpha, int64_t lda, double* out, 
     const cudaStream_t ss = p->pipe_s[i % ns];
     for (int l : units[i].wins) {
       const Window& w = p->win[l];
-      AFS_CUDA(cudaMemset2DAsync(p->grids + w.grid_off, sizeof(double) * p->grid_total, 0,
-                                 sizeof(double) * w.cells, R, ss));
+      if (det)
+        det_window_begin(p, w, R, ss);   // the limbs accumulate; finalize writes the grid
+      else
+        AFS_CUDA(cudaMemset2DAsync(p->grids + w.grid_off, sizeof(double) * p->grid_total, 0,
+                                   sizeof(double) * w.cells, R, ss));
     }
     spread_unit(p, units[i].wins, units[i].one_d, alpha, lda, R, ss);
+    if (det)
+      for (int l : units[i].wins) det_window_finalize(p, p->win[l], R, ss);
     spectral_windows(p, R, ss, units[i].wins);
     AFS_CUDA(cudaEventRecord(p->unit_ev[i], ss));
   }

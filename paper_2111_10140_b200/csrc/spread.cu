@@ -287,6 +287,52 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   AFS_CUDA(cudaGetLastError());
 }
 
+// deterministic mode in the window pipeline: the scale 2^S from max|alpha| once per apply,
+// then per window its limbs cleared before and converted after its spread
+void det_prepare(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
+  AFS_CUDA(cudaMemsetAsync(p->det_aux, 0, sizeof(double), s));
+  k_det_absmax<<<592, 256, 0, s>>>(alpha, lda, p->Ns, R,
+                                   reinterpret_cast<unsigned long long*>(p->det_aux));
+  k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound);
+  AFS_CUDA(cudaGetLastError());
+}
+
+// zero narr arrays (arr_stride apart) of R rows of `width` 8-byte words at `pitch` words: one
+// kernel instead of narr * R memset nodes (memsets are slow nodes inside a conditional body)
+__global__ void k_clear_rows(unsigned long long* __restrict__ base, int64_t arr_stride, int narr,
+                             int64_t pitch, int64_t width, int R) {
+  const int64_t tot = (int64_t)narr * R * width;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = i / (R * width), rem = i - a * R * width;
+    const int64_t r = rem / width, c = rem - r * width;
+    base[a * arr_stride + r * pitch + c] = 0ull;
+  }
+}
+
+void clear_rows(void* base, int64_t arr_stride, int narr, int64_t pitch, int64_t width, int R,
+                cudaStream_t s) {
+  const int64_t tot = (int64_t)narr * R * width;
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  k_clear_rows<<<std::max(1, blocks), 256, 0, s>>>(static_cast<unsigned long long*>(base),
+                                                   arr_stride, narr, pitch, width, R);
+}
+
+void det_window_begin(afs_plan* p, const Window& w, int R, cudaStream_t s) {
+  clear_rows(p->det_limbs + w.grid_off, p->grid_total * p->max_rhs, 3, p->grid_total, w.cells, R, s);
+}
+
+void det_window_finalize(afs_plan* p, const Window& w, int R, cudaStream_t s) {
+  const int64_t stride = p->grid_total * p->max_rhs;
+  for (int r = 0; r < R; ++r) {
+    const int64_t off = r * p->grid_total + w.grid_off;
+    k_det_finalize<<<(unsigned)((w.cells + 255) / 256), 256, 0, s>>>(p->det_limbs + off, stride,
+                                                                     w.cells, p->det_aux,
+                                                                     p->grids + off);
+  }
+  AFS_CUDA(cudaGetLastError());
+}
+
 void spread_unit(afs_plan* p, const std::vector<int>& wins, bool batch1d, const double* alpha,
                  int64_t lda, int R, cudaStream_t s) {
   if (batch1d) {   // the 1-D windows' solo spreads in shared launches (grids disjoint)
