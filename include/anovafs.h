@@ -159,11 +159,12 @@ int afs_plan_stage_times(afs_plan* plan, double* out4, int32_t reset);
  * applies; arrays of n_windows). */
 int afs_plan_window_times(afs_plan* plan, double* spread_ms, double* gather_ms, int32_t reset);
 
-/* Deterministic mode: the spread accumulates each grid cell in exact 108-bit fixed point
- * (three 36-bit limbs, 64-bit integer reductions) instead of fp64 atomics, with the scale
- * chosen per apply from max|alpha| so no partial sum can overflow; the limbs are converted
- * back to fp64 once.  Plans with more than 2^27 source nodes are rejected
- * (AFS_ERR_VALIDATION: limb headroom); a non-finite alpha yields NaN results.  afs_apply / afs_cg_solve then return bit-identical results run to run
+/* Deterministic mode: the spread accumulates each grid cell in exact fixed point -- three
+ * limbs of L bits (L = 40 for up to 2^23 source nodes, 36 up to 2^27) added with 64-bit
+ * integer reductions -- instead of fp64 atomics, with the scale chosen per apply from
+ * max|alpha| so no partial sum can overflow; the limbs are converted back to fp64 once.
+ * Plans with more than 2^27 source nodes are rejected (AFS_ERR_VALIDATION: limb headroom);
+ * a non-finite alpha yields NaN results.  afs_apply / afs_cg_solve then return bit-identical results run to run
  * for the same plan and inputs (the gather, spectral stage and CG reductions are already
  * fixed-order).  Costs 3x the grid memory for the limbs and ~2 extra passes per apply. */
 int afs_plan_set_deterministic(afs_plan* plan, int32_t enable);

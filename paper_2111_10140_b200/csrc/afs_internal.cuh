@@ -47,6 +47,7 @@ struct Window {
   int64_t det_stride = 0;           // grid_total * max_rhs
   const double* det_scale = nullptr;   // device [2]: 2^S, 2^-S for the current apply
   const double* det_base = nullptr;    // plan->grids (limb index = cell pointer - det_base)
+  double det_unit = 0.0, det_inv_unit = 0.0;   // 2^L, 2^-L for the plan's limb width L
 };
 
 struct SortedSide;   // geometry.cuh
@@ -115,6 +116,7 @@ struct afs_plan {
   int fft_mode = 0;                    // 0 four-step register FFT where n allows, 1 generic line kernel
   bool deterministic = false;          // fixed-point spread (afs_plan_set_deterministic)
   long long* det_limbs = nullptr;      // [3][grid_total * max_rhs]
+  int det_bits = 40;                   // limb width L: 40 for N <= 2^23, 36 up to 2^27
   double* det_aux = nullptr;           // [0] max|alpha| bits, [1] 2^S, [2] 2^-S
   double det_log2_bound = 0.0;         // log2(N * max window product) + margin
   std::vector<afs::GraphEntry> graphs;
@@ -204,12 +206,13 @@ int gather_branches(const afs_plan* p, int R);
 // ---------------------------------------------------------------------------
 // Default: one fp64 reduction (RED.E.ADD.F64); the summation order, hence the last bits,
 // depend on scheduling.  Deterministic mode: v * 2^S is split exactly into three signed
-// 36-bit limbs (|v 2^S| < 2^107 by the choice of S, k_det_scale) that are added with
+// L-bit limbs (|v 2^S| < 2^(3L-1) by the choice of S, k_det_scale) that are added with
 // 64-bit integer reductions -- associative, so the grid is bit-identical run to run.
-// A limb sum stays below 2^63 for up to 2^27 flushes into one cell; a cell receives at
-// most one flush per source node, and afs_plan_set_deterministic rejects N > 2^27.
-constexpr int kDetLimbBits = 36;
-constexpr int kDetTopBit = 3 * kDetLimbBits - 1;   // 107
+// A limb sum stays below 2^63 for up to 2^(63-L) flushes into one cell, and a cell receives
+// at most one flush per source node: the plan takes L = 40 bits (quantum 2^-119 of the bound)
+// for N <= 2^23 and L = 36 bits up to N = 2^27 (afs_plan_set_deterministic rejects more).
+// The wider limbs matter at large b*m: the window's tail values sit ~e^-(b m) below its peak,
+// so the fixed-point quantum must be far below the peak-based bound (fuzz: m = 6, os 1.5).
 __device__ __forceinline__ void grid_add(const Window& w, double* cell, double v) {
   if (w.det_limbs == nullptr) {
     atomicAdd(cell, v);
@@ -217,10 +220,12 @@ __device__ __forceinline__ void grid_add(const Window& w, double* cell, double v
   }
   const int64_t e = cell - w.det_base;
   const double x = v * __ldg(w.det_scale);
-  const double h = trunc(x * 0x1p-72);
-  const double r1 = fma(-h, 0x1p72, x);      // exact
-  const double m = trunc(r1 * 0x1p-36);
-  const double r2 = fma(-m, 0x1p36, r1);     // exact, |r2| < 2^36
+  const double u1 = w.det_unit, u2 = u1 * u1;                      // 2^L, 2^2L (exact)
+  const double i1 = w.det_inv_unit, i2 = i1 * i1;
+  const double h = trunc(x * i2);
+  const double r1 = fma(-h, u2, x);      // exact
+  const double m = trunc(r1 * i1);
+  const double r2 = fma(-m, u1, r1);     // exact, |r2| < 2^L
   const long long l0 = __double2ll_rn(r2), l1 = (long long)m, l2 = (long long)h;
   unsigned long long* L = reinterpret_cast<unsigned long long*>(w.det_limbs) + e;
   if (l0) atomicAdd(L, (unsigned long long)l0);

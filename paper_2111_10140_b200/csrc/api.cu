@@ -233,6 +233,8 @@ void refresh_det_windows(afs_plan* p) {
     w.det_stride = p->grid_total * p->max_rhs;
     w.det_scale = p->det_aux ? p->det_aux + 1 : nullptr;
     w.det_base = p->grids;
+    w.det_unit = std::ldexp(1.0, p->det_bits);
+    w.det_inv_unit = std::ldexp(1.0, -p->det_bits);
   }
   for (GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -277,6 +279,7 @@ static afs_plan* make_clone(afs_plan* p) {
     c->stage_streams = p->stage_streams;
     c->det_log2_bound = p->det_log2_bound;
     c->deterministic = p->deterministic;
+    c->det_bits = p->det_bits;
     c->mode_gen = p->mode_gen;
     AFS_CUDA(cudaMalloc(&c->grids, sizeof(double) * c->grid_total * c->max_rhs));
     if (c->scratch_a_len)
@@ -641,6 +644,7 @@ int afs_plan_set_deterministic(afs_plan* plan, int32_t enable) {
     }
     {
       std::lock_guard<std::mutex> lk(plan->pool_mu);
+      plan->det_bits = plan->Ns <= ((int64_t)1 << 23) ? 40 : 36;
       plan->deterministic = enable != 0;
       ++plan->mode_gen;   // clones made meanwhile are rebuilt at their next use
     }

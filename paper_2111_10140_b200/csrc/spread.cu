@@ -148,11 +148,12 @@ __global__ void k_det_absmax(const double* __restrict__ alpha, int64_t lda, int6
     atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-// S such that N * max|alpha| * max(window product) * 2^S < 2^107: every partial sum of a
-// cell fits the 108-bit limb range (log2_bound = log2(N * max product) + margin).  A
+// S such that N * max|alpha| * max(window product) * 2^S < 2^top_bit (top_bit = 3L - 1):
+// every partial sum of a cell fits the 3L-bit limb range (log2_bound = log2(N * max product)
+// + margin).  A
 // non-finite alpha (NaN marker from k_det_absmax) makes every grid value NaN, as the
 // fp64-atomic spread would propagate it.
-__global__ void k_det_scale(double* aux, double log2_bound) {
+__global__ void k_det_scale(double* aux, double log2_bound, int top_bit) {
   const double A = __longlong_as_double(*reinterpret_cast<const long long*>(aux));
   if (isnan(A)) {
     aux[1] = 0.0;
@@ -163,7 +164,7 @@ __global__ void k_det_scale(double* aux, double log2_bound) {
   if (A > 0.0) {
     int ea = 0;
     frexp(A, &ea);                      // A < 2^ea
-    S = kDetTopBit - (int)ceil(log2_bound) - ea;
+    S = top_bit - (int)ceil(log2_bound) - ea;
   }
   S = max(-1000, min(1000, S));
   aux[1] = ldexp(1.0, S);
@@ -172,11 +173,12 @@ __global__ void k_det_scale(double* aux, double log2_bound) {
 
 // exact 128-bit sum of the limbs, then one conversion (two roundings at most) and 2^-S
 __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stride, int64_t count,
-                               const double* __restrict__ aux, double* __restrict__ grids) {
+                               const double* __restrict__ aux, double* __restrict__ grids,
+                               int bits) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const __int128 v = ((__int128)limbs[2 * stride + i] << (2 * kDetLimbBits)) +
-                     ((__int128)limbs[stride + i] << kDetLimbBits) + (__int128)limbs[i];
+  const __int128 v = ((__int128)limbs[2 * stride + i] << (2 * bits)) +
+                     ((__int128)limbs[stride + i] << bits) + (__int128)limbs[i];
   const bool neg = v < 0;
   const unsigned __int128 u = (unsigned __int128)(neg ? -v : v);
   const double mag = __ull2double_rn((unsigned long long)(u >> 64)) * 0x1p64 +
@@ -228,7 +230,7 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
     AFS_CUDA(cudaMemsetAsync(p->det_aux, 0, sizeof(double), s));
     k_det_absmax<<<592, 256, 0, s>>>(alpha, lda, p->Ns, R,
                                      reinterpret_cast<unsigned long long*>(p->det_aux));
-    k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound);
+    k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound, 3 * p->det_bits - 1);
   } else {
     AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * cells, s));
   }
@@ -282,7 +284,7 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   if (det) {
     k_det_finalize<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
-        p->det_limbs, p->grid_total * p->max_rhs, cells, p->det_aux, p->grids);
+        p->det_limbs, p->grid_total * p->max_rhs, cells, p->det_aux, p->grids, p->det_bits);
   }
   AFS_CUDA(cudaGetLastError());
 }
@@ -293,7 +295,7 @@ void det_prepare(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStrea
   AFS_CUDA(cudaMemsetAsync(p->det_aux, 0, sizeof(double), s));
   k_det_absmax<<<592, 256, 0, s>>>(alpha, lda, p->Ns, R,
                                    reinterpret_cast<unsigned long long*>(p->det_aux));
-  k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound);
+  k_det_scale<<<1, 1, 0, s>>>(p->det_aux, p->det_log2_bound, 3 * p->det_bits - 1);
   AFS_CUDA(cudaGetLastError());
 }
 
@@ -328,7 +330,7 @@ void det_window_finalize(afs_plan* p, const Window& w, int R, cudaStream_t s) {
     const int64_t off = r * p->grid_total + w.grid_off;
     k_det_finalize<<<(unsigned)((w.cells + 255) / 256), 256, 0, s>>>(p->det_limbs + off, stride,
                                                                      w.cells, p->det_aux,
-                                                                     p->grids + off);
+                                                                     p->grids + off, p->det_bits);
   }
   AFS_CUDA(cudaGetLastError());
 }
