@@ -442,7 +442,11 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
           // dense 3-D windows take the tensor-core layout when padding the half-cells to groups
           // of 8 adds at most 15% nodes (tc3d.cuh); sparse ones keep the team kernels
           const bool tc3 = tc3_eligible(w.d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
+          // dense 2-D windows take the sub-cell layout (sc2d.cuh) when padding the sub-cells to
+          // groups of 8 adds at most 12% nodes; the others the half-cell layout (tc2d.cuh)
+          const bool scw = sc_eligible(w.d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
           auto build = [&](const double* X, int64_t N, SortedSide* side) {
+            if (scw && N >= 8 && build_sorted_side_sc(p, w, X, N, side, sc, 0.12)) return;
             if (tc) return build_sorted_side_tc(p, w, X, N, side, sc);
             if (tc3 && build_sorted_side_tc3(p, w, X, N, side, sc, 0.15)) return;
             build_sorted_side(p, w, X, N, side, sc);

@@ -4,6 +4,7 @@
 #define AFS_KB_DEFINE   // this translation unit owns the KB coefficient tables (kb_tables.inc)
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cub/cub.cuh>
 
 #include "geometry.cuh"
@@ -522,6 +523,160 @@ bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_
     out->chunk_cap = 0;
     p->device_bytes += (int64_t)(sizeof(double) * 3 + sizeof(int32_t)) * Npad +
                        (int64_t)sizeof(uint64_t) * (Npad / 8);
+    AFS_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  return true;
+}
+
+// ---- sub-cell layout for dense 2-D windows (sc2d.cuh) ---------------------------------------
+// Key: per dimension (u * 16 + s), u = floor(nx) mod n, s = floor(16 f); segments come from a
+// device run-length pass over the sorted keys, as in the 3-D layout above.
+__device__ __forceinline__ void sc_split(double nx, int n, int& u, int& s, double& t) {
+  const double fl = floor(nx);
+  const double f = nx - fl;                     // exact
+  const double f16 = f * (double)kScSub;        // exact (power of two)
+  const double sf = floor(f16);
+  long long uu = (long long)fl % n;
+  u = (int)(uu < 0 ? uu + n : uu);
+  s = (int)sf;
+  t = 2.0 * (f16 - sf) - 1.0;                   // exact: the sub-interval's Chebyshev variable
+}
+
+__global__ void k_prep_nodes_sc(const double* __restrict__ X, int64_t N, int dtot, Window w, int n,
+                                double* __restrict__ nx_out, uint64_t* __restrict__ key,
+                                int32_t* __restrict__ idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  uint64_t k = 0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const double xs = scaled_coord(X[j * dtot + w.feat[t]], w.center[t], w.scale);
+    const double nx = __dmul_rn((double)n, xs);   // nfft.py:170
+    nx_out[t * N + j] = nx;
+    int u, s;
+    double tv;
+    sc_split(nx, n, u, s, tv);
+    k = k * (uint64_t)(kScSub * n) + (uint64_t)(u * kScSub + s);
+  }
+  key[j] = k;
+  idx[j] = (int32_t)j;
+}
+
+__global__ void k_scatter_sc(const double* __restrict__ nx_in, const int32_t* __restrict__ idx,
+                             const int32_t* __restrict__ run_id, const int32_t* __restrict__ start,
+                             const int64_t* __restrict__ pad_start, int64_t N, int64_t Npad, int n,
+                             double* __restrict__ x_out, int32_t* __restrict__ perm,
+                             int32_t* __restrict__ ghdr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t r = run_id[i];
+  const int64_t dst = pad_start[r] + (i - start[r]);
+  const int32_t j = idx[i];
+  perm[dst] = j;
+  int u[2], sb[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    double tv;
+    sc_split(nx_in[t * N + j], n, u[t], sb[t], tv);
+    x_out[t * Npad + dst] = tv;
+  }
+  if ((dst & 7) == 0) ghdr[dst >> 3] = sc_header(u[0], u[1], sb[0], sb[1]);
+}
+
+// every group of a run starts with a node (only a run's last group is partial), so every group
+// holding nodes gets its header; padding slots keep the memset values (perm -1, t = 0)
+
+bool sc_eligible(int d, int m, int tab, int n, int64_t N) {
+  // 8-offset stencils (m = 4) on a compile-time table; 12-bit cells in the header (n <= 2048
+  // keeps the all-ones header unused); int32 node indices in the kernels
+  if (d != 2 || m != 4 || tab == 0 || n > 2048 || N < 8 || N >= (int64_t)INT32_MAX / 2) return false;
+  const char* e = getenv("AFS_TC");
+  if (e && e[0] == '0') return false;
+  const char* e2 = getenv("AFS_SC");   // A/B hook: AFS_SC=0 keeps the half-cell kernels
+  return !(e2 && e2[0] == '0');
+}
+
+bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                          BuildScratch& sc, double max_padding) {
+  const int n = p->n;
+  const cudaStream_t s = 0;
+  int bits = 1;
+  {
+    const long double keys = (long double)(kScSub * n) * (kScSub * n);
+    while ((long double)(1ULL << bits) < keys && bits < 63) ++bits;
+  }
+  if (const char* e = getenv("AFS_SC")) if (e[0] == '2') max_padding = 1e30;   // test hook: always
+  sc.reserve(N, 2);
+  const int th = 256;
+  const int64_t bl = (N + th - 1) / th;
+  k_prep_nodes_sc<<<bl, th, 0, s>>>(X, N, p->dtot, w, n, sc.nx_tmp, sc.key_a, sc.idx_a);
+  AFS_CUDA(cudaGetLastError());
+  size_t temp_bytes = 0;
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, sc.key_a, sc.key_b, sc.idx_a, sc.idx_b,
+                                           (int)N, 0, bits, s));
+  AFS_CUDA(cub::DeviceRadixSort::SortPairs(sc.sort_temp(temp_bytes), temp_bytes, sc.key_a, sc.key_b,
+                                           sc.idx_a, sc.idx_b, (int)N, 0, bits, s));
+  int32_t* head = reinterpret_cast<int32_t*>(sc.key_a);   // key_a is free: sorted keys are in key_b
+  int32_t* run_id = head + N;
+  k_run_heads<<<bl, th, 0, s>>>(sc.key_b, N, head);
+  AFS_CUDA(cudaGetLastError());
+  temp_bytes = 0;
+  AFS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, head, run_id, (int)N, s));
+  AFS_CUDA(cub::DeviceScan::InclusiveSum(sc.sort_temp(temp_bytes), temp_bytes, head, run_id, (int)N, s));
+  int32_t nruns = 0;
+  AFS_CUDA(cudaMemcpy(&nruns, run_id + N - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  k_minus1<<<bl, th, 0, s>>>(run_id, N);   // the inclusive scan counts runs from 1
+  AFS_CUDA(cudaGetLastError());
+  int32_t *start = nullptr, *padded = nullptr;
+  int64_t* pad_start = nullptr;
+  auto cleanup = [&] { cudaFree(start); cudaFree(padded); cudaFree(pad_start); };
+  try {
+    AFS_CUDA(cudaMalloc(&start, sizeof(int32_t) * nruns));
+    AFS_CUDA(cudaMalloc(&padded, sizeof(int32_t) * nruns));
+    AFS_CUDA(cudaMalloc(&pad_start, sizeof(int64_t) * (nruns + 1)));
+    k_run_bounds<<<bl, th, 0, s>>>(run_id, N, start, padded);
+    AFS_CUDA(cudaGetLastError());
+    k_run_pad<<<(unsigned)((nruns + th - 1) / th), th, 0, s>>>(start, padded, nruns);
+    AFS_CUDA(cudaGetLastError());
+    AFS_CUDA(cudaMemsetAsync(pad_start, 0, sizeof(int64_t), s));
+    temp_bytes = 0;
+    AFS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, padded, pad_start + 1, (int)nruns, s));
+    AFS_CUDA(cub::DeviceScan::InclusiveSum(sc.sort_temp(temp_bytes), temp_bytes, padded, pad_start + 1,
+                                           (int)nruns, s));
+    int64_t total = 0;
+    AFS_CUDA(cudaMemcpy(&total, pad_start + nruns, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (getenv("AFS_VERBOSE"))
+      fprintf(stderr, "[afs] sub-cell layout: N=%lld runs=%d padded=%lld (+%.1f%%) limit %.0f%%\n",
+              (long long)N, nruns, (long long)total, 100.0 * (double)(total - N) / (double)N,
+              100.0 * max_padding);
+    if ((double)(total - N) > max_padding * (double)N) {   // sparse: the half-cell kernels win
+      cleanup();
+      return false;
+    }
+    const int64_t ngroups = total / 8;
+    const int64_t Npad = total + 8 * kTcTailGroups;
+    AFS_CUDA(cudaMalloc(&out->nx, sizeof(double) * 2 * Npad));
+    AFS_CUDA(cudaMalloc(&out->perm, sizeof(int32_t) * Npad));
+    AFS_CUDA(cudaMalloc(&out->ghdr, sizeof(int32_t) * (Npad / 8)));
+    AFS_CUDA(cudaMemsetAsync(out->ghdr, 0, sizeof(int32_t) * (Npad / 8), s));
+    AFS_CUDA(cudaMemsetAsync(out->nx, 0, sizeof(double) * 2 * Npad, s));
+    AFS_CUDA(cudaMemsetAsync(out->perm, 0xff, sizeof(int32_t) * Npad, s));   // -1: no node
+    k_scatter_sc<<<bl, th, 0, s>>>(sc.nx_tmp, sc.idx_b, run_id, start, pad_start, N, Npad, n,
+                                   out->nx, out->perm, out->ghdr);
+    AFS_CUDA(cudaGetLastError());
+    out->N = Npad;
+    out->n_real = N;
+    out->ngroups = ngroups;
+    out->tc = true;
+    out->sc = true;
+    out->nchunks = 0;
+    out->chunk_cap = 0;
+    p->device_bytes += (int64_t)(sizeof(double) * 2 + sizeof(int32_t)) * Npad +
+                       (int64_t)sizeof(int32_t) * (Npad / 8);
     AFS_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
     cleanup();

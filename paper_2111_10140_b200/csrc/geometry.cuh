@@ -9,6 +9,7 @@ namespace afs {
 
 #include "kb_tables.inc"
 #include "kb_cheb.inc"
+#include "kb_sub.inc"
 
 constexpr int kPolyMaxOffsets = 2 * AFS_MAX_CUTOFF;   // 2m
 constexpr int kPolyTerms = 14;                        // degree 13 in x = f - 1/4
@@ -44,6 +45,10 @@ struct SortedSide {
   // x = (c ? 1 - f : f) - 1/4 of poly_weights instead of n*x, and ghdr[N/8] the group's
   // stencil (tc_header); N counts the padding, n_real does not
   bool tc = false;
+  // sub-cell layout (sc2d.cuh, dense 2-D windows; implies tc): sorted by (base cell,
+  // sub-interval floor(16 f)) per dimension, nx holds the Chebyshev variables 32 f - 2 s - 1,
+  // ghdr the group's sc_header
+  bool sc = false;
   int64_t n_real = 0;
   int32_t* ghdr = nullptr;
   uint64_t* ghdr64 = nullptr;   // 3-D layout: u0 | u1 << 16 | u2 << 32 | c_t << (48 + t)
@@ -80,7 +85,16 @@ bool tc3_eligible(int d, int m, int tab, int n, int64_t N);
 // half-cells to groups of 8 would add more than max_padding * N nodes
 bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
                            BuildScratch& sc, double max_padding);
-constexpr int kTcTailGroups = 32;   // >= the groups the kernels stage ahead (tc2d.cuh D * U)
+// dense 2-D windows: the sub-cell layout, or false (nothing built) when padding the sub-cells to
+// groups of 8 would add more than max_padding * N nodes
+bool sc_eligible(int d, int m, int tab, int n, int64_t N);
+bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
+                          BuildScratch& sc, double max_padding);
+constexpr int kScSub = 16;   // sub-intervals per cell and dimension (kb_sub.inc)
+__host__ __device__ __forceinline__ int32_t sc_header(int u0, int u1, int s0, int s1) {
+  return (int32_t)((uint32_t)u0 | ((uint32_t)u1 << 12) | ((uint32_t)s0 << 24) | ((uint32_t)s1 << 28));
+}
+constexpr int kTcTailGroups = 40;   // >= the groups the kernels read ahead (tc2d.cuh D * U; sc2d.cuh 8 batches + 3)
 
 // group header of the tensor-core layout: wrapped base cells and reflection classes
 __host__ __device__ __forceinline__ int32_t tc_header(int u0, int u1, int c0, int c1) {

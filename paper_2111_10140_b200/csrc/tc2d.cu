@@ -1,7 +1,7 @@
 // Launchers for the fp64 tensor-core 2-D kernels (tc2d.cuh).
 #include <cstdlib>
 
-#include "tc2d.cuh"
+#include "sc2d.cuh"
 
 namespace afs {
 
@@ -172,6 +172,10 @@ bool launch_spread_tc(const SortedSide& sv, const Window& w, int n, int tab, con
                       int64_t lda, int R, double* grid, int64_t rs, cudaStream_t s) {
   if (!sv.tc) return false;
   if (sv.ngroups == 0) return true;
+  if (sv.sc) {
+    launch_spread_sc(sv, w, n, tab, alpha, lda, R, grid, rs, s);
+    return true;
+  }
   if (tab == 1) spread_tab<1>(sv, w, n, alpha, lda, R, grid, rs, s);
   else if (tab == 2) spread_tab<2>(sv, w, n, alpha, lda, R, grid, rs, s);
   else throw Error(AFS_ERR_CUDA, "tensor-core layout without a compile-time KB table");
@@ -182,6 +186,10 @@ bool launch_gather_tc(const SortedSide& sv, const Window& w, int n, int tab, con
                       int64_t rs, int R, double* out, int64_t ldo, cudaStream_t s) {
   if (!sv.tc) return false;
   if (sv.ngroups == 0) return true;
+  if (sv.sc) {
+    launch_gather_sc(sv, w, n, tab, grid, rs, R, out, ldo, s);
+    return true;
+  }
   if (tab == 1) gather_tab<1>(sv, w, n, grid, rs, R, out, ldo, s);
   else if (tab == 2) gather_tab<2>(sv, w, n, grid, rs, R, out, ldo, s);
   else throw Error(AFS_ERR_CUDA, "tensor-core layout without a compile-time KB table");

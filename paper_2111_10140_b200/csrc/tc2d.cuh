@@ -146,6 +146,33 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
 }
+// L2 eviction policies (createpolicy): the node stream (x, perm, headers) is read once per
+// launch -> evict_first; the randomly indexed vector (alpha[perm], out[perm]: 80 MB at N = 1e7,
+// it fits the 126 MB L2) is re-read by every window -> evict_last, so its sectors stay
+// resident instead of being refetched from DRAM 32 bytes at a time.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void* dst, const void* src, uint64_t pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint(void* dst, const void* src, uint64_t pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double* ptr, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -171,6 +198,38 @@ __device__ __forceinline__ void tc_stage_nodes(TcRing<U, D, RG>& R, int st, cons
       else if constexpr (U == 2) cp_async8(&R.hdr[st][0], sv.ghdr + gb);
       else cp_async4(&R.hdr[st][0], sv.ghdr + gb);
     }
+  }
+}
+
+// tc_stage_nodes with an L2 policy on the 16-byte copies (U = 4)
+template <int U, int D, int RG>
+__device__ __forceinline__ void tc_stage_nodes_hint(TcRing<U, D, RG>& R, int st, const SortedSide& sv,
+                                                    int gb, int lane, uint64_t pol) {
+  static_assert(U == 4, "lane = node batches");
+  const int i0 = gb * 8;
+#pragma unroll
+  for (int c = lane; c < 10 * U + 1; c += 32) {
+    if (c < 4 * U) {
+      cp_async16_hint(&R.x0[st][2 * c], sv.x0() + i0 + 2 * c, pol);
+    } else if (c < 8 * U) {
+      cp_async16_hint(&R.x1[st][2 * (c - 4 * U)], sv.x1() + i0 + 2 * (c - 4 * U), pol);
+    } else if (c < 10 * U) {
+      cp_async16_hint(&R.perm[st][4 * (c - 8 * U)], sv.perm + i0 + 4 * (c - 8 * U), pol);
+    } else {
+      cp_async16_hint(&R.hdr[st][0], sv.ghdr + gb, pol);
+    }
+  }
+}
+
+// tc_stage_vals (one right-hand side) with an L2 policy on the random 8-byte copies
+template <int U, int D>
+__device__ __forceinline__ void tc_stage_vals_hint(TcRing<U, D, 1>& R, int st, const double* src,
+                                                   int lane, uint64_t pol) {
+#pragma unroll
+  for (int i = lane; i < 8 * U; i += 32) {
+    const int j = R.perm[st][i];
+    if (j >= 0) cp_async8_hint(&R.val[st][0][i], src + j, pol);
+    else R.val[st][0][i] = 0.0;
   }
 }
 
