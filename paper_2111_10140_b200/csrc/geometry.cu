@@ -439,15 +439,18 @@ __global__ void k_scatter_tc3(const double* __restrict__ nx_in, const int32_t* _
   if ((dst & 7) == 0) ghdr[dst >> 3] = h;
 }
 
-// Opt-in (AFS_TC3=1): measured on C4's clusters the tensor-core 3-D kernels are 6% faster than
-// the team kernels at N = 1e8 (110 vs 117 ms/matvec, R = 8) but slower at N = 1e7 (19.7 vs
-// 14.6 ms: the spread's per-half-cell flushes of 512 cells x R dominate shorter segments).
+// Default for dense windows: measured on C3's 3-D windows (N = 1e7, ~250 nodes per occupied
+// half-cell, one right-hand side) the tensor-core kernels take 0.79 / 0.82 ms against 0.86 /
+// 0.97 ms for the team kernels; on C4's clusters with 8 right-hand sides they are 6% faster at
+// N = 1e8 but slower at N = 1e7 (19.7 vs 14.6 ms: the spread flushes 512 cells x R per
+// half-cell and warp).  build_sorted_side_tc3 therefore also asks for >= 64 nodes per occupied
+// half-cell and right-hand side.  AFS_TC3=0/1 forces the choice (1: padding rule only).
 bool tc3_eligible(int d, int m, int tab, int n, int64_t N) {
   if (d != 3 || m != 4 || tab == 0 || n > 1024 || N < 8 || N >= (int64_t)INT32_MAX / 2) return false;
   const char* e = getenv("AFS_TC");
   if (e && e[0] == '0') return false;
   const char* e3 = getenv("AFS_TC3");
-  return e3 && e3[0] == '1';
+  return !(e3 && e3[0] == '0');
 }
 
 bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
@@ -500,7 +503,13 @@ bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_
                                            (int)nruns, s));
     int64_t total = 0;
     AFS_CUDA(cudaMemcpy(&total, pad_start + nruns, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    if ((double)(total - N) > max_padding * (double)N) {   // sparse: the FMA kernels win
+    bool dense = (double)(total - N) <= max_padding * (double)N;
+    {
+      const char* e3 = getenv("AFS_TC3");
+      const bool forced = e3 && e3[0] == '1';
+      if (!forced && (double)N < 64.0 * (double)p->max_rhs * (double)nruns) dense = false;
+    }
+    if (!dense) {   // sparse (or short half-cells per right-hand side): the FMA kernels win
       cleanup();
       return false;
     }

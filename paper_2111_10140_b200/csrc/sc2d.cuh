@@ -66,36 +66,6 @@ __host__ __device__ constexpr int sc_off(int k) {
 // in L2 across the windows) 2 ahead, coordinates and headers 2 ahead, the stencils of new
 // sub-cells 1 ahead.  Shared memory only holds the folded tables and the coefficient table.
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ double ldg_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double2 ldg_hint(const double2* p, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int2 ldg_hint(const int2* p, uint64_t pol) {
-  int2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-// random 8-byte load: no L1 allocation (a line would be used once), L2 policy
-__device__ __forceinline__ double ldg_rand(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void red_hint(double* p, double v, uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ int32_t ldg_hint(const int32_t* p, uint64_t pol) {
-  int32_t v;
-  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
 // the block's copy of the sub-interval coefficient table (16 x 8 x 8 doubles)
 template <int TAB>
 __device__ __forceinline__ void sc_load_coefs(double* csub) {

@@ -95,7 +95,7 @@ struct SoloPipe {
   __device__ __forceinline__ void load_val(const double* __restrict__ src, int64_t ld, int nr,
                                            int p, double (&v)[RG]) {
 #pragma unroll
-    for (int r = 0; r < RG; ++r) v[r] = (p >= 0 && r < nr) ? src[r * ld + p] : 0.0;
+    for (int r = 0; r < RG; ++r) v[r] = (src != nullptr && p >= 0 && r < nr) ? src[r * ld + p] : 0.0;
   }
   __device__ __forceinline__ void prime(const SortedSide& sv, const Chunk& ch, int lane,
                                         const double* __restrict__ src, int64_t ld, int nr) {
@@ -408,12 +408,12 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
     int cur = ch.cell0;
     const int count = ch.count;
     SoloPipe<D, RG> pipe;
-    pipe.prime(sv, ch, lane, out, ldo, nr);
+    pipe.prime(sv, ch, lane, nullptr, ldo, nr);   // no value prefetch: the result is added with RED
 #pragma unroll 1
     for (int q = lane; q < count; q += 32) {
       double nx[D];
-      double prior[RG];   // out[perm] before this window (each node is written once)
-      const int j = pipe.advance(sv, ch, q, nx, prior, out, ldo, nr);
+      double prior[RG];   // unused (zeros)
+      const int j = pipe.advance(sv, ch, q, nx, prior, nullptr, ldo, nr);
       const int u = wrap_cell((int)floor(nx[D - 1]), n);
       if (u != cur) {
         if (LOOKAHEAD && u == cur + 1 && ahead_cell == u + MM) {
@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(128) k_gather_solo(const SortedSide sv, const 
           }
           s = D == 2 ? fma(wt[0][ln], t0 + t1, s) : (t0 + t1);
         }
-        if (r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, s));
+        // one RED per node and launch (RN add in L2): the bits of load + add + store
+        if (r < nr) atomicAdd(out + r * ldo + j, __dmul_rn(w.eta, s));
       }
     }
     ch = chn;

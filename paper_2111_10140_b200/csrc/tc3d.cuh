@@ -31,14 +31,14 @@ struct TcRing3 {
 // node data of group g into slot st (16 B chunks: x0, x1, x2 four each, perm two, header 8 B)
 template <int DEPTH, int RG>
 __device__ __forceinline__ void tc3_stage_nodes(TcRing3<DEPTH, RG>& R, int st, const SortedSide& sv,
-                                                int g, int lane) {
+                                                int g, int lane, uint64_t pol) {
   const int i0 = g * 8;
   if (lane < 12) {
     const int t = lane >> 2, c = lane & 3;
-    cp_async16(&R.x[t][st][2 * c], sv.nx + t * sv.N + i0 + 2 * c);
+    cp_async16_hint(&R.x[t][st][2 * c], sv.nx + t * sv.N + i0 + 2 * c, pol);
   } else if (lane < 14) {
     const int c = lane - 12;
-    cp_async16(&R.perm[st][4 * c], sv.perm + i0 + 4 * c);
+    cp_async16_hint(&R.perm[st][4 * c], sv.perm + i0 + 4 * c, pol);
   } else if (lane == 14) {
     cp_async8(&R.hdr[st], sv.ghdr64 + g);
   }
@@ -47,12 +47,12 @@ __device__ __forceinline__ void tc3_stage_nodes(TcRing3<DEPTH, RG>& R, int st, c
 // per-node values src[r * ld + perm] of the group in slot st (its perm has landed); 0 for padding
 template <int DEPTH, int RG>
 __device__ __forceinline__ void tc3_stage_vals(TcRing3<DEPTH, RG>& R, int st, const double* src,
-                                               int64_t ld, int nr, int lane) {
+                                               int64_t ld, int nr, int lane, uint64_t pol) {
   if (lane < 8) {
     const int j = R.perm[st][lane];
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
-      if (j >= 0 && r < nr) cp_async8(&R.val[st][r][lane], src + r * ld + j);
+      if (j >= 0 && r < nr) cp_async8_hint(&R.val[st][r][lane], src + r * ld + j, pol);
       else R.val[st][r][lane] = 0.0;
     }
   }
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const W
   double cf[NKS];
   tc_coefs<TAB>(lane, cf);
   const double* g = grid + w.grid_off;
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
 
   // stencil operands B[k][n] = G[cell_x(o = 2k + t)][cell_y(p)][cell_z(r = n)], one per tile p
   double gf[RG][2][8];
@@ -102,13 +103,11 @@ __global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const W
 
 #pragma unroll
   for (int k = 0; k < DEPTH; ++k) {
-    tc3_stage_nodes(R, k, sv, g0 + k, lane);
+    tc3_stage_nodes(R, k, sv, g0 + k, lane, pol_stream);
     cp_async_commit();
   }
   cp_async_wait<DEPTH - 2>();
   __syncwarp();
-  tc3_stage_vals(R, 0, out, ldo, nr, lane);
-  tc3_stage_vals(R, 1, out, ldo, nr, lane);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
@@ -120,14 +119,10 @@ __global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const W
     const double x0 = R.x[0][st][slot], x1 = R.x[1][st][slot], x2 = R.x[2][st][slot];
     const int j = R.perm[st][slot];
     const uint64_t h = R.hdr[st];
-    double prior[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) prior[r] = R.val[st][r][slot];
     const int st1 = st + 1 == DEPTH ? 0 : st + 1;
     const int st2 = st1 + 1 == DEPTH ? 0 : st1 + 1;
     __syncwarp();
-    tc3_stage_nodes(R, st, sv, gi + DEPTH, lane);
-    tc3_stage_vals(R, st2, out, ldo, nr, lane);
+    tc3_stage_nodes(R, st, sv, gi + DEPTH, lane, pol_stream);
     cp_async_commit();
     if (h != hcur) {   // warp-uniform; dense segments span many groups
       load_stencil(h);
@@ -175,7 +170,9 @@ __global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const W
       double s = fma(fy[1], c[1], fy[0] * c[0]);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (q == 0 && j >= 0 && r < nr) out[r * ldo + j] = __dadd_rn(prior[r], __dmul_rn(w.eta, s));
+      // one reduction per node and launch (RN add in L2): the bits of load + add + store
+      // without the random load's round trip
+      if (q == 0 && j >= 0 && r < nr) red_hint(out + r * ldo + j, __dmul_rn(w.eta, s), pol_keep);
     }
     st = st1;
   }
@@ -204,6 +201,7 @@ __global__ void __launch_bounds__(128) k_spread_tc3(const SortedSide sv, const W
   double cf[NKS];
   tc_coefs<TAB>(lane, cf);
   double* g = grid + w.grid_off;
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
 
   double acc[RG][8][2];   // z-tile rr: lane holds G[o = slot][p = 2q + e][r = rr]
 #pragma unroll
@@ -230,13 +228,13 @@ __global__ void __launch_bounds__(128) k_spread_tc3(const SortedSide sv, const W
 
 #pragma unroll
   for (int k = 0; k < DEPTH; ++k) {
-    tc3_stage_nodes(R, k, sv, g0 + k, lane);
+    tc3_stage_nodes(R, k, sv, g0 + k, lane, pol_stream);
     cp_async_commit();
   }
   cp_async_wait<DEPTH - 2>();
   __syncwarp();
-  tc3_stage_vals(R, 0, alpha, lda, nr, lane);
-  tc3_stage_vals(R, 1, alpha, lda, nr, lane);
+  tc3_stage_vals(R, 0, alpha, lda, nr, lane, pol_keep);
+  tc3_stage_vals(R, 1, alpha, lda, nr, lane, pol_keep);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
@@ -257,8 +255,8 @@ __global__ void __launch_bounds__(128) k_spread_tc3(const SortedSide sv, const W
     const int st1 = st + 1 == DEPTH ? 0 : st + 1;
     const int st2 = st1 + 1 == DEPTH ? 0 : st1 + 1;
     __syncwarp();
-    tc3_stage_nodes(R, st, sv, gi + DEPTH, lane);
-    tc3_stage_vals(R, st2, alpha, lda, nr, lane);
+    tc3_stage_nodes(R, st, sv, gi + DEPTH, lane, pol_stream);
+    tc3_stage_vals(R, st2, alpha, lda, nr, lane, pol_keep);
     cp_async_commit();
     if (h != hcur) {   // warp-uniform
       if (hcur != ~0ULL) flush();
