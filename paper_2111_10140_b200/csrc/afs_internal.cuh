@@ -50,6 +50,10 @@ struct Window {
   double det_unit = 0.0, det_inv_unit = 0.0;   // 2^L, 2^-L for the plan's limb width L
 };
 
+// fraction of an SM's resident warps the next wave-sized launch (sc2d.cu, tc3d.cu) may take:
+// < 1 while two kernel classes are co-scheduled on two streams (spread.cu, gather.cu)
+extern thread_local double g_wave_share;
+
 struct SortedSide;   // geometry.cuh
 struct PolyTable;    // geometry.cuh
 
@@ -197,6 +201,7 @@ void cg_vec_update(double* x, double* r, const double* p, const double* ap, int6
 void cg_vec_direction(double* p, const double* r, int64_t n, double* ws, cudaStream_t s);
 void ensure_aux_streams(afs_plan* p);
 void fork_branches(afs_plan* p, int nb, cudaStream_t s);   // branches 1..nb-1 wait on s
+bool mix_classes(const afs_plan* p, double* share3, double* share2);   // spread.cu
 void join_branches(afs_plan* p, int nb, cudaStream_t s);   // s waits on branches 1..nb-1
 int spread_branches(const afs_plan* p);
 int gather_branches(const afs_plan* p, int R);

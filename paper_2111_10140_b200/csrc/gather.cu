@@ -185,7 +185,10 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
     // branches (as the spread, spread.cu): branch b > 0 accumulates its windows into the
     // plan's output buffer outx[b-1], added at the join -- out = sum over branches of the
     // windows' sums, each in window order (fixed, so run-to-run reproducible)
-    const int nb = timed ? 1 : gather_branches(p, R);
+    // plans holding both kernel classes run one class per branch (spread.cu mix_classes)
+    double share3 = 1.0, share2 = 1.0;
+    const bool mix = !timed && mix_classes(p, &share3, &share2);
+    const int nb = timed ? 1 : (mix ? 2 : gather_branches(p, R));
     if (nb > 1) {
       for (int b = 1; b < nb; ++b)
         if (!p->outx[b - 1]) {
@@ -207,7 +210,9 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
         }
     for (int l = 0; l < p->P; ++l) {
       if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
-      const int br = l % nb;
+      const bool heavy = mix && p->win[l].d == 3;
+      const int br = mix ? (heavy ? 1 : 0) : l % nb;
+      g_wave_share = mix ? (heavy ? share3 : share2) : 1.0;
       const cudaStream_t sl = br ? p->aux[br - 1] : s;
       double* o = br ? p->outx[br - 1] : out;
       const int64_t lo = br ? p->Nt : ldo;
@@ -217,6 +222,7 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
       }
       if (!gather_v2_window(p, l, o, lo, R, sl)) gather_v1(p, l, l + 1, o, lo, R, sl);
     }
+    g_wave_share = 1.0;
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
     if (nb > 1) {
       join_branches(p, nb, s);

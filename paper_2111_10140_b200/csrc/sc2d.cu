@@ -34,7 +34,9 @@ void wave(K kernel, int64_t ngroups, int& wps, int& gpw, int64_t& blocks) {
       wps = std::max(1, occ) * 4;
     }
   }
-  const int64_t warps = (int64_t)num_sms_sc() * wps;
+  // a share < 1 (co-scheduled classes) takes whole blocks: 4 warps each
+  const int use = std::max(4, (int)(wps * g_wave_share + 0.5) / 4 * 4);
+  const int64_t warps = (int64_t)num_sms_sc() * use;
   const int64_t gw = std::max<int64_t>(kU, (ngroups + warps - 1) / warps);
   gpw = (int)((gw + kU - 1) / kU * kU);
   blocks = ((ngroups + gpw - 1) / gpw * 32 + 127) / 128;

@@ -195,6 +195,8 @@ void ensure_aux_streams(afs_plan* p) {
   AFS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
 }
 
+thread_local double g_wave_share = 1.0;
+
 void fork_branches(afs_plan* p, int nb, cudaStream_t s) {
   ensure_aux_streams(p);
   AFS_CUDA(cudaEventRecord(p->ev_fork, s));
@@ -220,6 +222,30 @@ int spread_branches(const afs_plan* p) {
   return std::min(auto_branches(p), p->P);
 }
 
+// Co-scheduling of the two kernel classes (see spread_all): true when the plan holds
+// tensor-core 3-D windows and sub-cell 2-D windows and AFS_MIX=1.  Off by default: measured on
+// C3 (13.15 ms per matvec without) it costs 15.2-17.7 ms for shares 0.25-0.5 / 0.5-1.0 -- the
+// two classes' node streams and the evict_last vector compete for the L2.  AFS_MIX_SHARE3 /
+// AFS_MIX_SHARE2 set the shares.
+bool mix_classes(const afs_plan* p, double* share3, double* share2) {
+  if (p->window_eval != 0 || p->profiling) return false;
+  static const int mode = [] { const char* e = getenv("AFS_MIX"); return e ? atoi(e) : 0; }();
+  if (mode == 0) return false;
+  int n3 = 0, n2 = 0;
+  for (int l = 0; l < p->P; ++l) {
+    const SortedSide* sv = p->src_side[l];
+    if (!sv) return false;
+    if (p->win[l].d == 3 && sv->tc) ++n3;
+    if (p->win[l].d == 2 && sv->sc) ++n2;
+  }
+  if (n3 == 0 || n2 == 0) return false;
+  static const double s3 = [] { const char* e = getenv("AFS_MIX_SHARE3"); return e ? atof(e) : 0.25; }();
+  static const double s2 = [] { const char* e = getenv("AFS_MIX_SHARE2"); return e ? atof(e) : 0.75; }();
+  *share3 = s3;
+  *share2 = s2;
+  return true;
+}
+
 void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream_t s) {
   const bool det = p->deterministic && p->det_limbs;
   const int64_t cells = p->grid_total * R;
@@ -235,8 +261,13 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
     AFS_CUDA(cudaMemsetAsync(p->grids, 0, sizeof(double) * cells, s));
   }
   const bool timed = p->profiling && !p->wev_spread.empty();
-  // branches (not while timing windows): window l runs on branch l % nb
-  const int nb = timed ? 1 : spread_branches(p);
+  // branches (not while timing windows): window l runs on branch l % nb.  Plans that hold both
+  // kernel classes -- tensor-core 3-D windows (fp64-pipe-bound) and sub-cell 2-D windows
+  // (load/store-pipe-bound) -- run one class per branch, each with its share of the SM's
+  // resident warps, so the two kinds of warps share every SM (mix_classes)
+  double share3 = 1.0, share2 = 1.0;
+  const bool mix = !timed && mix_classes(p, &share3, &share2);
+  const int nb = timed ? 1 : (mix ? 2 : spread_branches(p));
   if (nb > 1) fork_branches(p, nb, s);
   // the 1-D windows' solo spreads share one launch (grids disjoint), at the first 1-D
   // window's place; AFS_SPREAD1D=0 keeps one launch per window
@@ -251,8 +282,10 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   for (int l = 0; l < p->P; ++l) {
     const Window& w = p->win[l];
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[l], s));
-    const int br = l % nb;
+    const bool heavy = mix && w.d == 3;
+    const int br = mix ? (heavy ? 1 : 0) : l % nb;
     const cudaStream_t sl = br ? p->aux[br - 1] : s;
+    g_wave_share = mix ? (heavy ? share3 : share2) : 1.0;
     if (!ones.empty() && w.d == 1) {
       if (l == ones[0]) {
         for (size_t b0 = 0; b0 < ones.size(); b0 += kSoloBatch) {
@@ -280,6 +313,7 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
       default: launch_spread_m<8>(p, w, alpha, lda, R, sl); break;
     }
   }
+  g_wave_share = 1.0;
   if (nb > 1) join_branches(p, nb, s);
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   if (det) {

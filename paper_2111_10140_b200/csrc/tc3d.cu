@@ -28,7 +28,8 @@ void launch_wave(K kernel, int64_t ngroups, int& warps_per_sm, int& gpw, int64_t
     AFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 128, 0));
     warps_per_sm = std::max(1, occ) * 4;
   }
-  const int64_t warps = (int64_t)sm_count() * warps_per_sm;
+  const int use = std::max(4, (int)(warps_per_sm * g_wave_share + 0.5) / 4 * 4);
+  const int64_t warps = (int64_t)sm_count() * use;
   gpw = (int)std::max<int64_t>(1, (ngroups + warps - 1) / warps);
   blocks = ((ngroups + gpw - 1) / gpw * 32 + 127) / 128;
 }
