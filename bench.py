@@ -608,9 +608,12 @@ def roofline(windows, win_sp, win_ga, N, R, M, m, n):
             "mean_launch_ms": t_launch * 1e3, "launches_per_step": len(times),
             "fp64": {"achieved_tflops": fp64, "peak_tflops": fpk, "frac": fp64 / fpk,
                      "peak_source": fpk_src, "fma_per_node": fpn},
-            "note": "m=4 makes the kernel fp64-pipe-bound (DESIGN.md §5); 2-D windows at m=4 run on "
-                    "the fp64 tensor cores (DMMA); traffic = ncu dram read+write per launch "
-                    "(profiles/ncu_traffic.json)"}
+            "note": "fp64 figures use the reference's tensor-product operation count (fma_per_node); "
+                    "the sub-cell 2-D kernels (sc2d.cuh) execute 62 (gather) / 78 (spread) per node and "
+                    "are bound by the SM load/store pipe: one l1tex cycle per randomly indexed 8-byte "
+                    "access plus the shared-memory tables (ncu, profiles/r02_ncu_sc_2d.txt); the 3-D "
+                    "kernels run on the fp64 tensor cores at ~71% of the pipe; traffic = ncu dram "
+                    "read+write per launch (profiles/ncu_traffic.json)"}
 
 
 def free_operator(afs, w, windows, weights, max_rhs=1, deterministic=False, device=None):

@@ -15,8 +15,12 @@ both through the same native stages as the fast summation:
   evaluates both at the nodes.
 
 Only the O(M^d) spectrum folding runs on the host; spread, transforms and
-gather run on the GPU.  The GPU plan needs equal bandwidths on all axes (one
-grid size per plan); the reference also allows unequal ones.
+gather run on the GPU.  The native plan has one grid size for all axes.  Unequal
+bandwidths (nfft.py:72-99, 139-177 allow them) are embedded in the largest one:
+the trigonometric sums are the same with the missing coefficients set to zero
+(forward) or dropped (adjoint), so the result approximates the same exact NDFT
+to the profile's accuracy -- it is not the reference's unequal-grid transform
+bit for bit (its window shape b_t = pi (2 - M_t / n_t) differs per axis).
 """
 
 from __future__ import annotations
@@ -53,9 +57,9 @@ class NfftPlan:
             grid = GridSpec(tuple(grid))
         profile = resolve_profile(profile)
         coords = validate_nodes(nodes, grid.dims)
-        M = grid.bandwidths[0]
-        if any(b != M for b in grid.bandwidths):
-            raise ValidationError("the GPU NfftPlan needs equal bandwidths on all axes")
+        M = max(grid.bandwidths)   # unequal bandwidths: embedded in the largest (module docstring)
+        self._embed = None if all(b == M for b in grid.bandwidths) else tuple(
+            slice(M // 2 - b // 2, M // 2 + b // 2) for b in grid.bandwidths)
         self.grid = grid
         self.profile = profile
         self.node_count = coords.shape[0]
@@ -124,7 +128,10 @@ class NfftPlan:
         out = []
         for part in (S[0], S[1]):
             out.append(np.where(pos, part[idx_p], np.conj(part[idx_n])))
-        return (out[0] + 1j * out[1]).ravel()
+        full = out[0] + 1j * out[1]
+        if self._embed is not None:   # keep I_{M_1} x ... x I_{M_d} of the embedding grid
+            full = full[self._embed]
+        return full.ravel()
 
     def forward(self, f_hat):
         """sum_k f_hat[k] exp(2 pi i <k, x_j>) at the plan's nodes."""
@@ -132,7 +139,11 @@ class NfftPlan:
         f_hat = self._check_coeffs(f_hat)
         d, M, n = self._d, self._M, self._n
         # deconvolve on I_M, pad to the pruned frequencies -M/2..M/2 (the +M/2 row is zero)
-        fh = f_hat.reshape((M,) * d)
+        if self._embed is None:
+            fh = f_hat.reshape((M,) * d)
+        else:                          # zero coefficients outside I_{M_1} x ... x I_{M_d}
+            fh = np.zeros((M,) * d, dtype=np.complex128)
+            fh[self._embed] = f_hat.reshape(self.grid.bandwidths)
         for t in range(d):
             fh = fh * self._deconv[:M].reshape((-1,) + (1,) * (d - 1 - t))
         P = np.zeros((M + 1,) * d, dtype=np.complex128)

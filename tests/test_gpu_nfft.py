@@ -105,3 +105,27 @@ def test_forward_cost_grows_at_most_linearly(afs):
     slope = np.polyfit(np.log(Ns), np.log(ts), 1)[0]
     print("times", dict(zip(Ns, ts)), "slope", slope)
     assert slope <= 1.15
+
+
+@pytest.mark.parametrize("bw", [(16, 8), (6, 12, 8), (4, 16)])
+def test_unequal_bandwidths_match_direct_sums(afs, bw):
+    """Unequal bandwidths (nfft.py:72-99 allows them) are embedded in the largest one; both
+    transforms against the oracle's direct sums at the profile's accuracy, and the adjoint
+    identity <forward(f), c> = <f, adjoint(c)> to roundoff of that accuracy."""
+    from oracle import fastsum_oracle as orc
+
+    rng = np.random.default_rng(sum(bw))
+    d = len(bw)
+    n_modes = int(np.prod(bw))
+    X = rng.uniform(-0.5, 0.5, size=(150, d))
+    f = rng.standard_normal(n_modes) + 1j * rng.standard_normal(n_modes)
+    c = rng.standard_normal(150) + 1j * rng.standard_normal(150)
+    plan = afs.NfftPlan(bw, X, "fine")
+    fwd, adj = plan.forward(f), plan.adjoint(c)
+    assert adj.shape == (n_modes,)
+    e_f = _rel(fwd, orc.ndft_forward(list(bw), X, f))
+    e_a = _rel(adj, orc.ndft_adjoint(list(bw), X, c))
+    print(f"bandwidths {bw}: forward {e_f:.2e}, adjoint {e_a:.2e}")
+    assert e_f < 1e-9 and e_a < 1e-9
+    lhs, rhs = np.vdot(c, fwd), np.vdot(adj, f)
+    assert abs(lhs - rhs) < 1e-8 * abs(lhs)
