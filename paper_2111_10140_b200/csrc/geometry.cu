@@ -658,11 +658,16 @@ bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t
                                            (int)nruns, s));
     int64_t total = 0;
     AFS_CUDA(cudaMemcpy(&total, pad_start + nruns, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    // dense enough: little padding and >= 64 nodes per occupied sub-cell (the spread folds and
+    // flushes 64 cells per sub-cell and warp: at C5's ~34 nodes per sub-cell it takes 0.065-0.08
+    // ms against 0.04 ms for the half-cell kernels; at C3's ~98 it is 25% faster)
+    const bool dense = (double)(total - N) <= max_padding * (double)N &&
+                       (max_padding > 1e29 || (double)N >= 64.0 * (double)nruns);
     if (getenv("AFS_VERBOSE"))
-      fprintf(stderr, "[afs] sub-cell layout: N=%lld runs=%d padded=%lld (+%.1f%%) limit %.0f%%\n",
-              (long long)N, nruns, (long long)total, 100.0 * (double)(total - N) / (double)N,
-              100.0 * max_padding);
-    if ((double)(total - N) > max_padding * (double)N) {   // sparse: the half-cell kernels win
+      fprintf(stderr, "[afs] sub-cell layout: N=%lld sub-cells=%d (%.1f nodes each) padding +%.1f%% -> %s\n",
+              (long long)N, nruns, (double)N / (double)nruns, 100.0 * (double)(total - N) / (double)N,
+              dense ? "sub-cell kernels" : "half-cell kernels");
+    if (!dense) {
       cleanup();
       return false;
     }
