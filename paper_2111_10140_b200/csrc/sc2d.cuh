@@ -130,44 +130,42 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
   const double2* px1 = reinterpret_cast<const double2*>(sv.x1() + (int64_t)g0 * 8) + lane;
   const int2* pperm = reinterpret_cast<const int2*>(sv.perm + (int64_t)g0 * 8) + lane;
   const int32_t* phdr = sv.ghdr + g0 + ug;
-  // pipeline registers, indexed by iteration mod depth (the loop is unrolled by 4, so the
-  // indices are compile-time and no register is moved -- a move would wait for its load):
-  // J perm (4 deep), A/B coordinates and H headers (2 deep)
-  int2 J[4];
+  // pipeline registers, two iterations deep, indexed by iteration parity (the loop is unrolled
+  // by 2, so the indices are compile-time and no register is moved -- a move would wait for
+  // its load): J perm, A/B coordinates, H headers
+  int2 J[2];
   double2 A[2], B[2];
   int32_t H[2];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) J[r] = ldg_hint(pperm + 32 * r, pol_stream);
-#pragma unroll
   for (int r = 0; r < 2; ++r) {
+    J[r] = ldg_hint(pperm + 32 * r, pol_stream);
     A[r] = ldg_hint(px0 + 32 * r, pol_stream);
     B[r] = ldg_hint(px1 + 32 * r, pol_stream);
     H[r] = __ldg(phdr + U * r);
   }
   int live = 0;   // table slot of the previous iteration's last group
 #pragma unroll 1
-  for (int gb4 = g0; gb4 < g1; gb4 += 4 * U) {
+  for (int gb2 = g0; gb2 < g1; gb2 += 2 * U) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (gb4 + r * U >= g1) break;   // warp-uniform
-      // this iteration's nodes, then refill their registers: perm of iteration + 4,
-      // coordinates and header of + 2
-      const double2 ta = A[r & 1], tb = B[r & 1];
+    for (int r = 0; r < 2; ++r) {
+      if (gb2 + r * U >= g1) break;   // warp-uniform
+      // this iteration's nodes, then refill their registers with iteration + 2
+      const double2 ta = A[r], tb = B[r];
       const int2 j = J[r];
-      const int32_t hl = H[r & 1];
+      const int32_t hl = H[r];
       pperm += 32;
       px0 += 32;
       px1 += 32;
       phdr += U;
-      J[r] = ldg_hint(pperm + 96, pol_stream);
-      A[r & 1] = ldg_hint(px0 + 32, pol_stream);
-      B[r & 1] = ldg_hint(px1 + 32, pol_stream);
-      H[r & 1] = __ldg(phdr + U);
+      J[r] = ldg_hint(pperm + 32, pol_stream);
+      A[r] = ldg_hint(px0 + 32, pol_stream);
+      B[r] = ldg_hint(px1 + 32, pol_stream);
+      H[r] = __ldg(phdr + U);
       __syncwarp();   // every lane is done reading the previous iteration's tables
       // tables of this iteration's new sub-cells go to the slots other than the live one
       int mine = live, cur = live, nnew = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {   // rolled: one copy of the fold keeps the loop in the i-cache
         const int32_t h = __shfl_sync(0xffffffffu, hl, 4 * u);
         if (h != hlast) {   // warp-uniform
           hlast = h;
@@ -256,7 +254,7 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
   const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   const int ug = lane >> 3;
 
-  // per-group moment accumulators: lane holds M[k = slot][l = 2q + e]
+  // per-group moment accumulators (independent DMMA chains): lane holds M[k = slot][l = 2q + e]
   double acc[U][2];
 #pragma unroll
   for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = 0.0;
@@ -298,38 +296,37 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
   const int32_t* pperm = sv.perm + (int64_t)g0 * 8 + lane;
   const int32_t* phdr = sv.ghdr + g0 + ug;
   auto ld_alpha = [&](int32_t j) { return j >= 0 ? ldg_rand(alpha + j, pol_keep) : 0.0; };
-  // pipeline registers, indexed by batch mod depth (loop unrolled by 4: compile-time indices,
-  // no register moves): perm 4 batches ahead, alpha[perm] 2 ahead, coordinates / headers 2 ahead
-  // (deeper did not help: the random loads are bound by the outstanding-miss capacity)
-  int32_t J[4];
+  // pipeline registers, two batches deep, indexed by batch parity (loop unrolled by 2:
+  // compile-time indices, no register moves): J holds the perm of batch + 2 (its alpha is
+  // requested now, used two batches later) and is refilled with batch + 4; deeper did not help
+  // (the random loads are bound by the outstanding-miss capacity)
+  int32_t J[2];
   double A[2], B[2], AL[2];
   int32_t H[2];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) J[r] = ldg_hint(pperm + 32 * r, pol_stream);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     A[r] = ldg_hint(px0 + 32 * r, pol_stream);
     B[r] = ldg_hint(px1 + 32 * r, pol_stream);
     H[r] = __ldg(phdr + 4 * r);
+    AL[r] = ld_alpha(ldg_hint(pperm + 32 * r, pol_stream));
+    J[r] = ldg_hint(pperm + 32 * (r + 2), pol_stream);
   }
-  AL[0] = ld_alpha(J[0]);
-  AL[1] = ld_alpha(J[1]);
 #pragma unroll 1
-  for (int gb4 = g0; gb4 < g1; gb4 += 4 * U) {
+  for (int gb2 = g0; gb2 < g1; gb2 += 2 * U) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (gb4 + r * U >= g1) break;   // warp-uniform
-      const double t0 = A[r & 1], t1 = B[r & 1], al = AL[r & 1];
-      const int32_t hl = H[r & 1];
+    for (int r = 0; r < 2; ++r) {
+      if (gb2 + r * U >= g1) break;   // warp-uniform
+      const double t0 = A[r], t1 = B[r], al = AL[r];
+      const int32_t hl = H[r];
       pperm += 32;
       px0 += 32;
       px1 += 32;
       phdr += 4;
-      J[r] = ldg_hint(pperm + 96, pol_stream);
-      A[r & 1] = ldg_hint(px0 + 32, pol_stream);
-      B[r & 1] = ldg_hint(px1 + 32, pol_stream);
-      H[r & 1] = __ldg(phdr + 4);
-      AL[r & 1] = ld_alpha(J[(r + 2) & 3]);
+      A[r] = ldg_hint(px0 + 32, pol_stream);
+      B[r] = ldg_hint(px1 + 32, pol_stream);
+      H[r] = __ldg(phdr + 4);
+      AL[r] = ld_alpha(J[r]);                        // batch + 2
+      J[r] = ldg_hint(pperm + 96, pol_stream);       // batch + 4
       __syncwarp();   // every lane is done reading the previous batch's vectors
       {   // this lane's node: alpha T_k(t0) and T_l(t1), k, l < 8, into the transposed tables
         const double u2 = 2.0 * t0, v2 = 2.0 * t1;
