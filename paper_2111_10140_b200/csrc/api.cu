@@ -445,17 +445,31 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
           // dense 2-D windows take the sub-cell layout (sc2d.cuh) when padding the sub-cells to
           // groups of 8 adds at most 12% nodes; the others the half-cell layout (tc2d.cuh)
           const bool scw = sc_eligible(w.d, p->m, p->kb_tab, p->n, std::max(p->Ns, p->Nt));
-          auto build = [&](const double* X, int64_t N, SortedSide* side) {
+          // 3-D windows with several right-hand sides (C4: R = 8): the team kernels spread 4
+          // right-hand sides per pass and win the spread (41.7 vs 47.8 ms at N = 1e8), the
+          // tensor-core kernels win the gather (48.8 vs 61.5 ms).  Their source side therefore keeps
+          // the team layout and the gather gets its own tensor-core layout of the same nodes
+          // (3.25 x 8 N bytes more).  AFS_DUAL3=0 keeps one layout.
+          bool dual3 = tc3 && p->max_rhs >= 3;
+          if (const char* e = getenv("AFS_DUAL3")) dual3 = dual3 && e[0] != '0';
+          auto build = [&](const double* X, int64_t N, SortedSide* side, bool spread_side) {
             if (scw && N >= 8 && build_sorted_side_sc(p, w, X, N, side, sc, 0.12)) return;
             if (tc) return build_sorted_side_tc(p, w, X, N, side, sc);
-            if (tc3 && build_sorted_side_tc3(p, w, X, N, side, sc, 0.15)) return;
+            if (tc3 && !(dual3 && spread_side) &&
+                build_sorted_side_tc3(p, w, X, N, side, sc, 0.15, spread_side && !dual3))
+              return;
             build_sorted_side(p, w, X, N, side, sc);
           };
           p->src_side[l] = new SortedSide();
-          build(p->src, p->Ns, p->src_side[l]);
+          build(p->src, p->Ns, p->src_side[l], true);
+          if (dual3 && !p->has_targets) {
+            SortedSide* gs = new SortedSide();
+            if (build_sorted_side_tc3(p, w, p->src, p->Ns, gs, sc, 0.15, false)) p->tgt_side[l] = gs;
+            else delete gs;
+          }
           if (p->has_targets) {
             p->tgt_side[l] = new SortedSide();
-            build(p->tgt, p->Nt, p->tgt_side[l]);
+            build(p->tgt, p->Nt, p->tgt_side[l], false);
           }
         }
         AFS_CUDA(cudaDeviceSynchronize());
@@ -510,7 +524,11 @@ int afs_plan_get_info(const afs_plan* plan, afs_plan_info* info) {
     info->n_targets = plan->Nt;
     info->kernel_launches_per_apply = plan->launches_per_apply;
     int tcw = 0;
-    for (const afs::SortedSide* sv : plan->src_side) tcw += (sv && sv->tc) ? 1 : 0;
+    for (size_t l = 0; l < plan->src_side.size(); ++l) {   // either side (a gather-only layout counts)
+      const afs::SortedSide* sv = plan->src_side[l];
+      const afs::SortedSide* gv = l < plan->tgt_side.size() ? plan->tgt_side[l] : nullptr;
+      tcw += ((sv && sv->tc) || (gv && gv->tc)) ? 1 : 0;
+    }
     info->tensor_core_windows = tcw;
   });
 }

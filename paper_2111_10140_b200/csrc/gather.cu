@@ -113,7 +113,8 @@ static void gather_v1(afs_plan* p, int l0, int l1, double* out, int64_t ldo, int
 static bool gather_v2_window(afs_plan* p, int l, double* out, int64_t ldo, int R, cudaStream_t s) {
   if (p->window_eval != 0) return false;
   const Window& w = p->win[l];
-  const SortedSide& sv = p->has_targets ? *p->tgt_side[l] : *p->src_side[l];
+  // the target side, or a gather-only layout of the sources (api.cu), else the source side
+  const SortedSide& sv = p->tgt_side[l] ? *p->tgt_side[l] : *p->src_side[l];
   if (sv.tc && w.d == 3)
     return launch_gather_tc3(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);
   if (sv.tc) return launch_gather_tc(sv, w, p->n, p->kb_tab, p->grids, p->grid_total, R, out, ldo, s);

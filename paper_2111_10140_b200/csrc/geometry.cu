@@ -454,7 +454,7 @@ bool tc3_eligible(int d, int m, int tab, int n, int64_t N) {
 }
 
 bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
-                           BuildScratch& sc, double max_padding) {
+                           BuildScratch& sc, double max_padding, bool for_spread) {
   const int n = p->n;
   const cudaStream_t s = 0;
   int bits = 1;
@@ -507,7 +507,8 @@ bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_
     {
       const char* e3 = getenv("AFS_TC3");
       const bool forced = e3 && e3[0] == '1';
-      if (!forced && (double)N < 64.0 * (double)p->max_rhs * (double)nruns) dense = false;
+      // (the per-right-hand-side rule is about the spread's flushes; a gather-only side skips it)
+      if (for_spread && !forced && (double)N < 64.0 * (double)p->max_rhs * (double)nruns) dense = false;
     }
     if (!dense) {   // sparse (or short half-cells per right-hand side): the FMA kernels win
       cleanup();

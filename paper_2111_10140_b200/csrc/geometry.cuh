@@ -84,7 +84,7 @@ bool tc3_eligible(int d, int m, int tab, int n, int64_t N);
 // dense 3-D windows: the tensor-core layout, or false (nothing built) when padding the
 // half-cells to groups of 8 would add more than max_padding * N nodes
 bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
-                           BuildScratch& sc, double max_padding);
+                           BuildScratch& sc, double max_padding, bool for_spread = true);
 // dense 2-D windows: the sub-cell layout, or false (nothing built) when padding the sub-cells to
 // groups of 8 would add more than max_padding * N nodes
 bool sc_eligible(int d, int m, int tab, int n, int64_t N);

@@ -40,7 +40,7 @@ bool pipeline_applies(const afs_plan* p) {
   int n1 = 0;
   for (int l = 0; l < p->P; ++l) {
     if (p->win[l].d != 1) continue;
-    if (p->src_side[l]->tc || (p->has_targets && p->tgt_side[l]->tc)) return false;
+    if (p->src_side[l]->tc || (p->tgt_side[l] && p->tgt_side[l]->tc)) return false;
     ++n1;
   }
   if (n1 == 1) return false;
