@@ -115,6 +115,9 @@ struct afs_plan {
   int window_eval = 0;                 // 0 polynomial window + sliding kernels, 1 exact mirror (v1)
   int kb_tab = 0;                      // compile-time KB table id (kb_table_id)
   std::vector<afs::SortedSide*> src_side, tgt_side;
+  // 1-D windows: unwrapped base-cell range [lo, lo + cnt) of the target nodes (gather1d.cu
+  // sub-interval tables); cnt = 0 when not computed
+  std::vector<int> cell1_lo, cell1_cnt;
   afs::PolyTable* poly = nullptr;      // host copy (passed by value to kernels)
   bool use_graphs = true;
   int fft_mode = 0;                    // 0 four-step register FFT where n allows, 1 generic line kernel
@@ -202,6 +205,7 @@ void cg_vec_direction(double* p, const double* r, int64_t n, double* ws, cudaStr
 void ensure_aux_streams(afs_plan* p);
 void fork_branches(afs_plan* p, int nb, cudaStream_t s);   // branches 1..nb-1 wait on s
 bool mix_classes(const afs_plan* p, double* share3, double* share2);   // spread.cu
+void gather_1d_cell_ranges(afs_plan* p);   // gather1d.cu: fills cell1_lo / cell1_cnt at plan time
 void join_branches(afs_plan* p, int nb, cudaStream_t s);   // s waits on branches 1..nb-1
 int spread_branches(const afs_plan* p);
 int gather_branches(const afs_plan* p, int R);

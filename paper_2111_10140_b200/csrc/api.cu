@@ -273,6 +273,8 @@ static afs_plan* make_clone(afs_plan* p) {
     c->kb_tab = p->kb_tab;
     c->src_side = p->src_side;
     c->tgt_side = p->tgt_side;
+    c->cell1_lo = p->cell1_lo;
+    c->cell1_cnt = p->cell1_cnt;
     c->poly = p->poly;
     c->use_graphs = p->use_graphs;
     c->fft_mode = p->fft_mode;
@@ -472,6 +474,7 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
             build(p->tgt, p->Nt, p->tgt_side[l], false);
           }
         }
+        gather_1d_cell_ranges(p);
         AFS_CUDA(cudaDeviceSynchronize());
       } catch (...) {
         sc.release();

@@ -8,7 +8,15 @@
 // written once for all 1-D windows, coalesced, instead of one scattered read-modify-write
 // per window.  Same window values (poly_weights) and cell/fraction arithmetic as the
 // sorted kernels, so the spread's nx and the gather's agree bit for bit.
+//
+// At m = 4 on a compile-time table the window values are not evaluated per node at all
+// (k_gather_1d_sub): every block folds each window's grid into per-half-cell Chebyshev tables in
+// shared memory, Ghat[c][h][k] = sum_o Cc[o][k] g[c - 3 + o] (kb_cheb.inc, 12 terms), over the
+// cells the target nodes occupy (the fast summation scales them into ~0.22 n cells: 6 KB per
+// window, so all of C5's 20 windows stay in one pass over the nodes), and a node costs its
+// table row (96 bytes) and 22 FMAs instead of 8 twelve-term polynomials.
 #include <algorithm>
+#include <climits>
 
 #include "afs_internal.cuh"
 #include "geometry.cuh"
@@ -72,6 +80,197 @@ __global__ void __launch_bounds__(256) k_gather_1d_fused(const double* __restric
   }
 }
 
+// ---- per-cell Chebyshev tables (m = 4, compile-time KB table) ------------------------------
+constexpr int kMax1dSub = 32;       // windows per launch
+constexpr int kMaxCells1d = 96;     // occupied cells per window the tables may cover
+constexpr int kRow1d = 12;          // Chebyshev terms per half-cell (kb_cheb.inc)
+constexpr int kRowPad1d = 14;       // table row stride: 112 bytes = 28 banks, so random rows spread over 8 bank groups
+
+struct Win1s {
+  int feat;
+  double center, scale, eta;
+  int64_t grid_off;
+  int cell_lo, ncell;   // unwrapped base cells [cell_lo, cell_lo + ncell) of the target nodes
+  int tab_off;          // doubles, into the block's tables
+  int gs_off;           // doubles, into the block's staged grid slices
+};
+
+struct Gather1dSubBatch {
+  int nwin;
+  int tab_total, gs_total;
+  Win1s w[kMax1dSub];
+};
+
+__device__ __forceinline__ int mod_cell(int v, int n) {
+  int r = v % n;
+  return r < 0 ? r + n : r;
+}
+
+// Ghat[c][h][k] = sum_o Cc[h ? 7 - o : o][k] g[c - 3 + o]: the half-cell series of tc2d.cuh in
+// one dimension (h: the reflection class f > 1/2, variable u = 4 ((h ? 1 - f : f) - 1/4))
+template <int TAB>
+__global__ void __launch_bounds__(512) k_gather_1d_sub(const double* __restrict__ Z, int64_t N, int dtot,
+                                                       int n, const Gather1dSubBatch B,
+                                                       const double* __restrict__ grid,
+                                                       double* __restrict__ out) {
+  extern __shared__ double sm[];   // Cc[8][12] | grid slices | tables
+  double* cc = sm;
+  double* gs = sm + 8 * kRow1d;
+  double* tab = gs + B.gs_total;
+  for (int i = threadIdx.x; i < 8 * kRow1d; i += blockDim.x) cc[i] = kb_cheb<TAB>(i / kRow1d, i % kRow1d);
+  for (int l = 0; l < B.nwin; ++l) {   // the stencil cells of the occupied range: cell_lo - 3 ...
+    const Win1s& w = B.w[l];
+    for (int i = threadIdx.x; i < w.ncell + 7; i += blockDim.x)
+      gs[w.gs_off + i] = __ldg(grid + w.grid_off + mod_cell(w.cell_lo - 3 + i, n));
+  }
+  __syncthreads();
+  for (int l = 0; l < B.nwin; ++l) {
+    const Win1s& w = B.w[l];
+    const double* g = gs + w.gs_off;
+    for (int e = threadIdx.x; e < w.ncell * 2 * kRow1d; e += blockDim.x) {
+      const int k = e % kRow1d, ch = e / kRow1d, h = ch & 1, c = ch >> 1;
+      double v = 0.0;
+#pragma unroll
+      for (int o = 0; o < 8; ++o) v = fma(cc[(h ? 7 - o : o) * kRow1d + k], g[c + o], v);
+      tab[w.tab_off + ch * kRowPad1d + k] = v;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = out[i];
+    const double* zrow = Z + i * dtot;
+#pragma unroll 1
+    for (int l = 0; l < B.nwin; ++l) {
+      const Win1s& w = B.w[l];
+      const double nx = __dmul_rn((double)n, scaled_coord(__ldg(zrow + w.feat), w.center, w.scale));
+      const double fl = floor(nx);
+      const double f = nx - fl;   // exact
+      const bool refl = f > 0.5;
+      const double t = 4.0 * ((refl ? __dsub_rn(1.0, f) : f) - 0.25);   // as poly_weights' x, times 4
+      const int c = (int)fl - w.cell_lo;      // in [0, ncell) by gather_1d_cell_ranges
+      const double2* row = reinterpret_cast<const double2*>(tab + w.tab_off + (c * 2 + (refl ? 1 : 0)) * kRowPad1d);
+      // sum_k Ghat_k T_k(t), recurrence in t
+      const double t2 = 2.0 * t;
+      double2 cf = row[0];
+      double tm = 1.0, tk = t;
+      double s = fma(cf.y, t, cf.x);
+#pragma unroll
+      for (int j = 1; j < kRow1d / 2; ++j) {
+        cf = row[j];
+        double tn = fma(t2, tk, -tm);
+        tm = tk;
+        tk = tn;
+        s = fma(cf.x, tk, s);
+        tn = fma(t2, tk, -tm);
+        tm = tk;
+        tk = tn;
+        s = fma(cf.y, tk, s);
+      }
+      acc = __dadd_rn(acc, __dmul_rn(w.eta, s));
+    }
+    out[i] = acc;
+  }
+}
+
+// min / max of floor(n x~) over the target nodes of one window
+__global__ void k_cell_range(const double* __restrict__ Z, int64_t N, int dtot, int feat, double center,
+                             double scale, int n, int* __restrict__ lohi) {
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)floor(__dmul_rn((double)n, scaled_coord(Z[i * dtot + feat], center, scale)));
+    lo = min(lo, c);
+    hi = max(hi, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(lohi, lo);
+    atomicMax(lohi + 1, hi);
+  }
+}
+
+void gather_1d_cell_ranges(afs_plan* p) {
+  p->cell1_lo.assign(p->P, 0);
+  p->cell1_cnt.assign(p->P, 0);
+  if (p->window_eval != 0 || p->m != 4 || (p->kb_tab != 1 && p->kb_tab != 2)) return;
+  std::vector<int> ws;
+  for (int l = 0; l < p->P; ++l)
+    if (p->win[l].d == 1) ws.push_back(l);
+  if (ws.size() < 2) return;
+  int* d = nullptr;
+  AFS_CUDA(cudaMalloc(&d, sizeof(int) * 2 * ws.size()));
+  std::vector<int> h(2 * ws.size());
+  for (size_t i = 0; i < ws.size(); ++i) h[2 * i] = INT_MAX, h[2 * i + 1] = INT_MIN;
+  AFS_CUDA(cudaMemcpy(d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice));
+  const double* Z = p->has_targets ? p->tgt : p->src;
+  const int blocks = (int)std::min<int64_t>((p->Nt + 255) / 256, 148 * 4);
+  for (size_t i = 0; i < ws.size(); ++i) {
+    const Window& w = p->win[ws[i]];
+    k_cell_range<<<std::max(1, blocks), 256>>>(Z, p->Nt, p->dtot, w.feat[0], w.center[0], w.scale, p->n,
+                                               d + 2 * i);
+  }
+  AFS_CUDA(cudaGetLastError());
+  AFS_CUDA(cudaMemcpy(h.data(), d, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  for (size_t i = 0; i < ws.size(); ++i) {
+    if (h[2 * i] > h[2 * i + 1]) continue;
+    p->cell1_lo[ws[i]] = h[2 * i];
+    p->cell1_cnt[ws[i]] = h[2 * i + 1] - h[2 * i] + 1;
+  }
+}
+
+// every 1-D window has a computed cell range small enough for the tables
+static bool gather_1d_sub_ok(const afs_plan* p) {
+  if (p->window_eval != 0 || p->m != 4 || (p->kb_tab != 1 && p->kb_tab != 2)) return false;
+  if (const char* e = getenv("AFS_GATHER1D"))
+    if (e[0] == '1') return false;   // A/B hook: the 12-term per-node kernel
+  if ((int)p->cell1_cnt.size() != p->P) return false;
+  for (int l = 0; l < p->P; ++l)
+    if (p->win[l].d == 1 && (p->cell1_cnt[l] < 1 || p->cell1_cnt[l] > kMaxCells1d)) return false;
+  return true;
+}
+
+static void gather_1d_sub(afs_plan* p, const std::vector<int>& ws, double* out, int64_t ldo, int R,
+                          cudaStream_t s) {
+  const double* Z = p->has_targets ? p->tgt : p->src;
+  const size_t budget = 190 * 1024 - sizeof(double) * 8 * kRow1d;
+  size_t i0 = 0;
+  while (i0 < ws.size()) {
+    Gather1dSubBatch B{};
+    size_t bytes = 0;
+    while (i0 + B.nwin < ws.size() && B.nwin < kMax1dSub) {
+      const int l = ws[i0 + B.nwin];
+      const Window& w = p->win[l];
+      const int nc = p->cell1_cnt[l];
+      const size_t need = sizeof(double) * ((size_t)nc * 2 * kRowPad1d + nc + 8);
+      if (B.nwin > 0 && bytes + need > budget) break;
+      B.w[B.nwin] = Win1s{w.feat[0], w.center[0], w.scale, w.eta, w.grid_off, p->cell1_lo[l], nc,
+                          B.tab_total, B.gs_total};
+      B.tab_total += nc * 2 * kRowPad1d;
+      B.gs_total += (nc + 7 + 1) & ~1;   // keep the tables 16-byte aligned
+      bytes += need;
+      ++B.nwin;
+    }
+    const size_t smem = sizeof(double) * (8 * kRow1d + B.gs_total + B.tab_total);
+    auto launch = [&](auto k) {
+      AFS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t blocks = std::min<int64_t>((p->Nt + 511) / 512, 148);
+      for (int r = 0; r < R; ++r)
+        k<<<(unsigned)std::max<int64_t>(1, blocks), 512, smem, s>>>(Z, p->Nt, p->dtot, p->n, B,
+                                                                    p->grids + r * p->grid_total,
+                                                                    out + r * ldo);
+    };
+    if (p->kb_tab == 1) launch(k_gather_1d_sub<1>);
+    else launch(k_gather_1d_sub<2>);
+    i0 += B.nwin;
+  }
+}
+
 template <int MM, int TAB, int RG>
 static void launch_1d(afs_plan* p, const Gather1dBatch& B, double* out, int64_t ldo, int nr,
                       const double* grids, cudaStream_t s) {
@@ -120,6 +319,11 @@ void gather_1d_fused(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t 
   std::vector<int> ws;
   for (int l = 0; l < p->P; ++l)
     if (p->win[l].d == 1) ws.push_back(l);
+  if (gather_1d_sub_ok(p)) {
+    gather_1d_sub(p, ws, out, ldo, R, s);
+    AFS_CUDA(cudaGetLastError());
+    return;
+  }
   const size_t per_win = sizeof(double) * 2 * p->n;   // RG <= 2
   const int fit = (int)std::min<size_t>(kMax1d, (160 * 1024) / per_win);
   for (size_t b0 = 0; b0 < ws.size(); b0 += fit) {
