@@ -189,8 +189,27 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
     // plans holding both kernel classes run one class per branch (spread.cu mix_classes)
     double share3 = 1.0, share2 = 1.0;
     const bool mix = !timed && mix_classes(p, &share3, &share2);
-    const int nb = timed ? 1 : (mix ? 2 : gather_branches(p, R));
-    if (nb > 1) {
+    int nb = timed ? 1 : (mix ? 2 : gather_branches(p, R));
+    // Vectors too large for private accumulators (C3: 80 MB): outside deterministic mode the
+    // sorted gathers of different windows may share `out` across branches -- each adds its
+    // result with one RED per node, so concurrent windows only change the order of the adds
+    // (run-to-run variation of the last bits, as the atomic spread already has).  The fused 1-D
+    // gather (plain read-modify-write) runs before the fork.  AFS_GATHER_SHARED=0 disables it.
+    bool shared_out = false;
+    if (nb == 1 && !timed && !mix && !p->deterministic && p->P >= 2) {
+      static const bool on = [] { const char* e = getenv("AFS_GATHER_SHARED"); return !(e && e[0] == '0'); }();
+      bool all_red = on;
+      for (int l = 0; l < p->P && all_red; ++l) {
+        const SortedSide& sv = p->tgt_side[l] ? *p->tgt_side[l] : *p->src_side[l];
+        if (!sv.tc && v2_rhs_group(p->win[l].d, p->m, R, false) < 1) all_red = false;
+      }
+      if (all_red) {
+        shared_out = true;
+        nb = std::min(p->P, p->stage_streams > 0 ? p->stage_streams : 3);
+        if (nb < 2) shared_out = false, nb = 1;
+      }
+    }
+    if (nb > 1 && !shared_out) {
       for (int b = 1; b < nb; ++b)
         if (!p->outx[b - 1]) {
           AFS_CUDA(cudaMalloc(&p->outx[b - 1], sizeof(double) * p->Nt * p->max_rhs));
@@ -209,23 +228,28 @@ void gather_all(afs_plan* p, double* out, int64_t ldo, int R, cudaStream_t s) {
           fused[l] = 1;
           if (first1d < 0) first1d = l;
         }
+    if (shared_out) {   // the 1-D windows first (not atomic), then the fork
+      if (first1d >= 0) gather_1d_fused(p, out, ldo, R, s);
+      fork_branches(p, nb, s);
+    }
     for (int l = 0; l < p->P; ++l) {
       if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[l], s));
       const bool heavy = mix && p->win[l].d == 3;
       const int br = mix ? (heavy ? 1 : 0) : l % nb;
       g_wave_share = mix ? (heavy ? share3 : share2) : 1.0;
       const cudaStream_t sl = br ? p->aux[br - 1] : s;
-      double* o = br ? p->outx[br - 1] : out;
-      const int64_t lo = br ? p->Nt : ldo;
+      double* o = (br && !shared_out) ? p->outx[br - 1] : out;
+      const int64_t lo = (br && !shared_out) ? p->Nt : ldo;
       if (fused[l]) {
-        if (l == first1d) gather_1d_fused(p, o, lo, R, sl);
+        if (l == first1d && !shared_out) gather_1d_fused(p, o, lo, R, sl);
         continue;
       }
       if (!gather_v2_window(p, l, o, lo, R, sl)) gather_v1(p, l, l + 1, o, lo, R, sl);
     }
     g_wave_share = 1.0;
     if (timed) AFS_CUDA(cudaEventRecord(p->wev_gather[p->P], s));
-    if (nb > 1) {
+    if (nb > 1 && shared_out) join_branches(p, nb, s);
+    if (nb > 1 && !shared_out) {
       join_branches(p, nb, s);
       const int64_t tot = p->Nt * R;
       const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);

@@ -210,11 +210,11 @@ void join_branches(afs_plan* p, int nb, cudaStream_t s) {
   }
 }
 
-// Large windows (C3: 0.2-1 ms kernels) gain most of the overlap from 2 branches; small ones
+// Large windows (C3: 0.12-0.8 ms kernels) gain most of the overlap from 2-3 branches; small ones
 // (C5 at N=1M: ~25 us kernels, tail-dominated) from 4.
 static int auto_branches(const afs_plan* p) {
   if (p->stage_streams > 0) return p->stage_streams;
-  return p->Ns * (int64_t)p->P <= (int64_t)64 << 20 ? 4 : 2;
+  return p->Ns * (int64_t)p->P <= (int64_t)64 << 20 ? 4 : 3;   // C3: 13.76 / 13.00 / 12.97 / 12.97 ms for 1-4
 }
 
 int spread_branches(const afs_plan* p) {
