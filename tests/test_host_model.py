@@ -127,3 +127,42 @@ def test_windowset_rules():
     with pytest.raises(ValidationError):
         WindowSet([])
     assert WindowSet([(0, 1, 2), (3,)]).weights == (0.5, 0.5)
+
+
+def _parse_inc_tables(path, shape):
+    """Arrays of a generated csrc/*.inc table file, in file order."""
+    import re
+
+    text = open(path).read()
+    tables = []
+    for body in re.findall(r"AFS_KB_INIT\(\{(.*?)\}\)\);", text, flags=re.S):
+        vals = [float(v) for v in re.findall(r"[-+]?\d+\.?\d*(?:[eE][-+]?\d+)?", body)]
+        tables.append(np.array(vals).reshape(shape))
+    return tables
+
+
+def test_sub_cell_tables_reproduce_the_reference_window():
+    """csrc/kb_sub.inc (tools/gen_kb_sub.py): on every sub-interval f in [s/16, (s+1)/16) the
+    8-term Chebyshev series in t = 32 f - 2 s - 1 gives the reference's window value
+    phi(f + 3 - o) (nfft.py:118-122) for every stencil offset, for both compile-time ratios
+    n/M = 2 and 3/2; the reference formula itself carries ~3.5e-15 of the peak in fp64."""
+    from oracle import fastsum_oracle as orc
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    inc = os.path.join(os.path.dirname(here), "paper_2111_10140_b200", "csrc", "kb_sub.inc")
+    tabs = _parse_inc_tables(inc, (16, 8, 8))
+    assert len(tabs) == 2
+    rng = np.random.default_rng(0)
+    for tab, (M, n) in zip(tabs, ((64, 128), (64, 96))):
+        b = orc.kb_shape(M, n)
+        peak = float(orc.kb_window(np.array([0.0]), 4, b)[0])
+        worst = 0.0
+        for s in range(16):
+            t = rng.uniform(-1.0, 1.0, size=64)
+            f = (s + (t + 1.0) / 2.0) / 16.0
+            T = np.cos(np.arange(8)[:, None] * np.arccos(t)[None, :])     # T_k(t)
+            for o in range(8):
+                got = tab[s, o] @ T
+                want = orc.kb_window(f + 3 - o, 4, b)
+                worst = max(worst, float(np.abs(got - want).max()) / peak)
+        assert worst < 2e-14, worst
