@@ -163,17 +163,23 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
       H[r] = __ldg(phdr + U);
       __syncwarp();   // every lane is done reading the previous iteration's tables
       // tables of this iteration's new sub-cells go to the slots other than the live one
+      // groups that start a new sub-cell: one ballot instead of walking the 8 headers
+      const int32_t hprev = __shfl_up_sync(0xffffffffu, hl, 4);
+      const bool first = q == 0 && (lane < 4 ? hl != hlast : hl != hprev);
+      unsigned cm = __ballot_sync(0xffffffffu, first);   // bit 4u: group u starts a new sub-cell
+      hlast = __shfl_sync(0xffffffffu, hl, 28);
+      // the lane's table: the live one, or the (i-th new) slot of the last change up to its group
+      const int before = __popc(cm & ((2u << (lane | 3)) - 1u));
       int mine = live, cur = live, nnew = 0;
+      if (before > 0) mine = (before - 1) < live ? (before - 1) : before;
 #pragma unroll 1
-      for (int u = 0; u < U; ++u) {   // rolled: one copy of the fold keeps the loop in the i-cache
-        const int32_t h = __shfl_sync(0xffffffffu, hl, 4 * u);
-        if (h != hlast) {   // warp-uniform
-          hlast = h;
-          cur = nnew < live ? nnew : nnew + 1;
-          ++nnew;
-          fold(h, tab + cur * kScTab);
-        }
-        if (ug == u) mine = cur;
+      while (cm) {   // usually no or one new sub-cell per iteration
+        const int bit = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const int32_t h = __shfl_sync(0xffffffffu, hl, bit);
+        cur = nnew < live ? nnew : nnew + 1;
+        ++nnew;
+        fold(h, tab + cur * kScTab);
       }
       live = cur;
       __syncwarp();
