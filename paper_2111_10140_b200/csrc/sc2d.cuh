@@ -226,8 +226,12 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
       }
       // each node is written once per launch and launches on one vector are ordered, so the
       // reduction (RN add in L2, no load round trip) gives the bits of load + add + store
+#ifdef AFS_SC_NO_RED   // measurement only: the gather without its output traffic
+      if (j.x == -12345) red_hint(out, sa + sb, pol_keep);
+#else
       if (j.x >= 0) red_hint(out + j.x, __dmul_rn(w.eta, sa), pol_keep);
       if (j.y >= 0) red_hint(out + j.y, __dmul_rn(w.eta, sb), pol_keep);
+#endif
     }
   }
 }
