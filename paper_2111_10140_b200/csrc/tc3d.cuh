@@ -14,6 +14,11 @@
 
 #include "tc2d.cuh"
 
+// __launch_bounds__ min blocks per SM of the 3-D tensor-core kernels (tuning hook)
+#ifndef AFS_TC3_MINB
+#define AFS_TC3_MINB 5
+#endif
+
 namespace afs {
 
 __device__ __forceinline__ int tc3_u(uint64_t h, int t) { return (int)((h >> (16 * t)) & 0xffff); }
@@ -62,7 +67,7 @@ __device__ __forceinline__ void tc3_stage_vals(TcRing3<DEPTH, RG>& R, int st, co
 // gather: out[perm] += eta * interp over groups [g0, g1) of one warp
 // ----------------------------------------------------------------------------
 template <int RG, int TAB, bool POW2, int DEPTH>
-__global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, RG == 1 ? AFS_TC3_MINB : 1) k_gather_tc3(const SortedSide sv, const Window w, int n,
                                                     const double* __restrict__ grid,
                                                     int64_t rhs_stride, int nr,
                                                     double* __restrict__ out, int64_t ldo, int gpw) {
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(128) k_gather_tc3(const SortedSide sv, const W
 // MMA accumulators (8 z-tiles of D[o][p]) and flushed when the group header changes
 // ----------------------------------------------------------------------------
 template <int RG, int TAB, bool POW2, int DEPTH>
-__global__ void __launch_bounds__(128) k_spread_tc3(const SortedSide sv, const Window w, int n,
+__global__ void __launch_bounds__(128, RG == 1 ? AFS_TC3_MINB : 1) k_spread_tc3(const SortedSide sv, const Window w, int n,
                                                     const double* __restrict__ alpha, int64_t lda,
                                                     int nr, double* __restrict__ grid,
                                                     int64_t rhs_stride, int gpw) {
