@@ -51,6 +51,10 @@ __device__ __forceinline__ int sc_cell(int u, int o, int n) {
 }
 
 constexpr int kScTab = 40;     // kept coefficients per sub-cell
+#ifndef AFS_SC_GDEPTH
+#define AFS_SC_GDEPTH 2
+#endif
+constexpr int kScGatherDepth = AFS_SC_GDEPTH;   // register pipeline depth of the gather (iterations; <= 4: the layout's tail)
 constexpr int kScGatherU = 8;  // groups per gather iteration (two adjacent nodes per lane)
 __host__ __device__ constexpr int sc_rowlen(int k) { return 8 - 2 * (k / 2); }
 __host__ __device__ constexpr int sc_off(int k) {
@@ -130,14 +134,15 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
   const double2* px1 = reinterpret_cast<const double2*>(sv.x1() + (int64_t)g0 * 8) + lane;
   const int2* pperm = reinterpret_cast<const int2*>(sv.perm + (int64_t)g0 * 8) + lane;
   const int32_t* phdr = sv.ghdr + g0 + ug;
-  // pipeline registers, two iterations deep, indexed by iteration parity (the loop is unrolled
-  // by 2, so the indices are compile-time and no register is moved -- a move would wait for
-  // its load): J perm, A/B coordinates, H headers
-  int2 J[2];
-  double2 A[2], B[2];
-  int32_t H[2];
+  // pipeline registers, kScGatherDepth iterations deep, indexed by iteration mod depth (the loop
+  // is unrolled by the depth, so the indices are compile-time and no register is moved -- a
+  // move would wait for its load): J perm, A/B coordinates, H headers
+  constexpr int PD = kScGatherDepth;
+  int2 J[PD];
+  double2 A[PD], B[PD];
+  int32_t H[PD];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < PD; ++r) {
     J[r] = ldg_hint(pperm + 32 * r, pol_stream);
     A[r] = ldg_hint(px0 + 32 * r, pol_stream);
     B[r] = ldg_hint(px1 + 32 * r, pol_stream);
@@ -145,11 +150,11 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
   }
   int live = 0;   // table slot of the previous iteration's last group
 #pragma unroll 1
-  for (int gb2 = g0; gb2 < g1; gb2 += 2 * U) {
+  for (int gbd = g0; gbd < g1; gbd += PD * U) {
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (gb2 + r * U >= g1) break;   // warp-uniform
-      // this iteration's nodes, then refill their registers with iteration + 2
+    for (int r = 0; r < PD; ++r) {
+      if (gbd + r * U >= g1) break;   // warp-uniform
+      // this iteration's nodes, then refill their registers with iteration + depth
       const double2 ta = A[r], tb = B[r];
       const int2 j = J[r];
       const int32_t hl = H[r];
@@ -157,10 +162,10 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_GATHER) k_gather_sc(
       px0 += 32;
       px1 += 32;
       phdr += U;
-      J[r] = ldg_hint(pperm + 32, pol_stream);
-      A[r] = ldg_hint(px0 + 32, pol_stream);
-      B[r] = ldg_hint(px1 + 32, pol_stream);
-      H[r] = __ldg(phdr + U);
+      J[r] = ldg_hint(pperm + 32 * (PD - 1), pol_stream);
+      A[r] = ldg_hint(px0 + 32 * (PD - 1), pol_stream);
+      B[r] = ldg_hint(px1 + 32 * (PD - 1), pol_stream);
+      H[r] = __ldg(phdr + U * (PD - 1));
       __syncwarp();   // every lane is done reading the previous iteration's tables
       // tables of this iteration's new sub-cells go to the slots other than the live one
       // groups that start a new sub-cell: one ballot instead of walking the 8 headers
