@@ -4,7 +4,7 @@ The reference has no parallelism.  The path shards naturally
 in one exchange step per matvec:
 
 * ``WindowSharded`` (C3/C5: many windows) — windows are dealt to ranks by
-  LPT on their spread+gather cost ``N (2m)^d_l``; every rank holds all
+  LPT on their modelled spread+gather time (``window_costs``); every rank holds all
   points and alpha, computes ``sum_{l in S_rank} eta_l K_l alpha`` and one
   all-reduce sums the N-vector partials.  The terms are independent
   (anova.py:179-183), so the result equals the single-GPU sum up to the
@@ -49,19 +49,23 @@ def lpt_assign(costs, world):
 
 
 def window_costs(windows, N, m):
-    """Modelled spread+gather time of each window: N x fp64 work per node / pipe efficiency.
+    """Modelled spread+gather time of each window on one B200.
 
-    Work per node and pass = touches (2m)^d + window values 2m d 12 (12-term polynomials)
-    + line products (2m)^(d-1); efficiency 0.74 for the tensor-core 2-D kernels (m = 4),
-    0.58 for the FMA kernels (profiles/r01_ncu_final.txt).  At m = 4 this prices a 3-D
-    window at 4.2 2-D windows, as measured on C3 (1.86 vs 0.47 ms); the bare touch count
-    (N (2m)^d) would say 8 and leave the 8-rank deal of C3 at 83% balance."""
+    At m = 4 the measured per-node times of the kernels each window gets:
+    3-D 155 ps (tensor-core kernels), 2-D 25 ps when the window is dense enough for the sub-cell
+    kernels (about N >= 5e6) and 73 ps on the half-cell kernels, 1-D 20 ps (batched / fused).  C3
+    prices a 3-D window at 6.2 2-D windows (1.55 vs 0.248 ms at N = 1e7); the bare touch count
+    N (2m)^d would say 8.  Other cutoffs: fp64 work per node and pass -- touches (2m)^d + window
+    values 2m d 12 + line products (2m)^(d-1) -- over the FMA kernels' pipe efficiency 0.58."""
     costs = []
     for w in windows:
         d = len(w)
-        work = (2 * m) ** d + 2 * m * d * 12 + (2 * m) ** (d - 1)
-        eff = 0.74 if (d == 2 and m == 4) else 0.58
-        costs.append(float(N) * work / eff)
+        if m == 4:
+            ps = {1: 20.0, 2: 25.0 if N >= 5_000_000 else 73.0, 3: 155.0}[d]
+            costs.append(float(N) * ps)
+        else:
+            work = (2 * m) ** d + 2 * m * d * 12 + (2 * m) ** (d - 1)
+            costs.append(float(N) * work / 0.58)
     return costs
 
 
