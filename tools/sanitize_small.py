@@ -2,7 +2,8 @@
 
     compute-sanitizer --tool memcheck python tools/sanitize_small.py
 covers 1-D/2-D/3-D windows, the tensor-core 2-D kernels (window-matrix and, forced on here,
-Chebyshev), the (AFS_TC3=1) 3-D tensor-core kernels, targets, multi-RHS, the per-window
+Chebyshev; the sub-cell kernels in a second, forced pass), the (AFS_TC3=1) 3-D tensor-core kernels,
+the table-based fused 1-D gather, targets, multi-RHS, the per-window
 pipeline, deterministic mode, the device CG (whole-solve graph, fused cooperative epilogue),
 concurrent applies on workspace clones, apply_complex and the sharded-CG vector kernels."""
 import os
@@ -31,6 +32,16 @@ for tgt in (None, Z):
     y = op.apply(A)
     y1 = op.apply(A[:, 0])
     print("rhs consistency", float(np.max(np.abs(y[:, 0] - y1))))
+# the sub-cell 2-D kernels (forced regardless of density) and two 1-D windows (fused table gather)
+os.environ["AFS_SC"] = "2"
+for tgt in (None, Z):
+    ops = afs.AnovaKernelOperator(X, [(3, 4), (1, 4), (5,), (0,)], 0.3, prof, tgt, cfg, strict=False, max_rhs=3)
+    ys = ops.apply(A)
+    os.environ["AFS_SC"] = "0"
+    oph = afs.AnovaKernelOperator(X, [(3, 4), (1, 4), (5,), (0,)], 0.3, prof, tgt, cfg, strict=False, max_rhs=3)
+    os.environ["AFS_SC"] = "2"
+    print("sub-cell vs half-cell kernels", float(np.max(np.abs(ys - oph.apply(A))) / np.max(np.abs(ys))))
+os.environ.pop("AFS_SC")
 det = afs.AnovaKernelOperator(X, windows, 0.3, prof, None, cfg, strict=False, max_rhs=3, deterministic=True)
 det.apply(A)
 res = afs.cg_solve(afs.KernelSystem(det, 0.5), A[:, 1], tol=1e-8, maxiter=30)
