@@ -206,16 +206,21 @@ void gather_1d_cell_ranges(afs_plan* p) {
   AFS_CUDA(cudaMalloc(&d, sizeof(int) * 2 * ws.size()));
   std::vector<int> h(2 * ws.size());
   for (size_t i = 0; i < ws.size(); ++i) h[2 * i] = INT_MAX, h[2 * i + 1] = INT_MIN;
-  AFS_CUDA(cudaMemcpy(d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice));
-  const double* Z = p->has_targets ? p->tgt : p->src;
-  const int blocks = (int)std::min<int64_t>((p->Nt + 255) / 256, 148 * 4);
-  for (size_t i = 0; i < ws.size(); ++i) {
-    const Window& w = p->win[ws[i]];
-    k_cell_range<<<std::max(1, blocks), 256>>>(Z, p->Nt, p->dtot, w.feat[0], w.center[0], w.scale, p->n,
-                                               d + 2 * i);
+  try {
+    AFS_CUDA(cudaMemcpy(d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice));
+    const double* Z = p->has_targets ? p->tgt : p->src;
+    const int blocks = (int)std::min<int64_t>((p->Nt + 255) / 256, 148 * 4);
+    for (size_t i = 0; i < ws.size(); ++i) {
+      const Window& w = p->win[ws[i]];
+      k_cell_range<<<std::max(1, blocks), 256>>>(Z, p->Nt, p->dtot, w.feat[0], w.center[0], w.scale, p->n,
+                                                 d + 2 * i);
+    }
+    AFS_CUDA(cudaGetLastError());
+    AFS_CUDA(cudaMemcpy(h.data(), d, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+  } catch (...) {
+    cudaFree(d);
+    throw;
   }
-  AFS_CUDA(cudaGetLastError());
-  AFS_CUDA(cudaMemcpy(h.data(), d, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
   cudaFree(d);
   for (size_t i = 0; i < ws.size(); ++i) {
     if (h[2 * i] > h[2 * i + 1]) continue;
