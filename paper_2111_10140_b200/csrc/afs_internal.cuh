@@ -48,6 +48,9 @@ struct Window {
   const double* det_scale = nullptr;   // device [2]: 2^S, 2^-S for the current apply
   const double* det_base = nullptr;    // plan->grids (limb index = cell pointer - det_base)
   double det_unit = 0.0, det_inv_unit = 0.0;   // 2^L, 2^-L for the plan's limb width L
+  // 2^((d_max - d) e), e = floor(log2 phi(0)): lifts a lower-dimensional window's values to the
+  // plan-wide bound N max|alpha| phi(0)^d_max the scale 2^S is chosen for (undone at finalize)
+  double det_boost = 1.0;
 };
 
 // fraction of an SM's resident warps the next wave-sized launch (sc2d.cu, tc3d.cu) may take:
@@ -126,6 +129,7 @@ struct afs_plan {
   int det_bits = 40;                   // limb width L: 40 for N <= 2^23, 36 up to 2^27
   double* det_aux = nullptr;           // [0] max|alpha| bits, [1] 2^S, [2] 2^-S
   double det_log2_bound = 0.0;         // log2(N * max window product) + margin
+  int det_dmax = 1, det_peak_exp = 0;  // largest window dimension; floor(log2 phi(0)) (per-window boost)
   std::vector<afs::GraphEntry> graphs;
   cudaStream_t istream = nullptr;   // plan-owned stream (graph capture needs a non-legacy one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -228,7 +232,7 @@ __device__ __forceinline__ void grid_add(const Window& w, double* cell, double v
     return;
   }
   const int64_t e = cell - w.det_base;
-  const double x = v * __ldg(w.det_scale);
+  const double x = (v * w.det_boost) * __ldg(w.det_scale);   // both factors are powers of two
   const double u1 = w.det_unit, u2 = u1 * u1;                      // 2^L, 2^2L (exact)
   const double i1 = w.det_inv_unit, i2 = i1 * i1;
   const double h = trunc(x * i2);

@@ -235,6 +235,7 @@ void refresh_det_windows(afs_plan* p) {
     w.det_base = p->grids;
     w.det_unit = std::ldexp(1.0, p->det_bits);
     w.det_inv_unit = std::ldexp(1.0, -p->det_bits);
+    w.det_boost = std::ldexp(1.0, (p->det_dmax - w.d) * p->det_peak_exp);
   }
   for (GraphEntry& g : p->graphs)   // captured graphs hold the old window parameters
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -280,6 +281,8 @@ static afs_plan* make_clone(afs_plan* p) {
     c->fft_mode = p->fft_mode;
     c->stage_streams = p->stage_streams;
     c->det_log2_bound = p->det_log2_bound;
+    c->det_dmax = p->det_dmax;
+    c->det_peak_exp = p->det_peak_exp;
     c->deterministic = p->deterministic;
     c->det_bits = p->det_bits;
     c->mode_gen = p->mode_gen;
@@ -392,6 +395,8 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
       const double peak = std::sinh(p->b * p->m) / (3.141592653589793 * p->m);   // phi(0)
       p->det_log2_bound = std::log2((double)std::max<int64_t>(p->Ns, 1)) +
                           dmax * std::log2(std::max(peak, 1.0)) + 2.0;
+      p->det_dmax = dmax;
+      p->det_peak_exp = (int)std::floor(std::log2(std::max(peak, 1.0)));
     }
     p->launches_per_apply = launches;
 

@@ -171,10 +171,13 @@ __global__ void k_det_scale(double* aux, double log2_bound, int top_bit) {
   aux[2] = ldexp(1.0, -S);
 }
 
-// exact 128-bit sum of the limbs, then one conversion (two roundings at most) and 2^-S
+// exact 128-bit sum of the limbs, then one conversion (two roundings at most), 2^-S and the
+// window's boost undone.  wins != nullptr: cells of all windows ([rhs][grid_total]), the window
+// looked up by its grid offset; else one window with the given inverse boost.
 __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stride, int64_t count,
                                const double* __restrict__ aux, double* __restrict__ grids,
-                               int bits) {
+                               int bits, const Window* __restrict__ wins, int P, int64_t grid_total,
+                               int dmax, int peak_exp, double inv_boost) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const __int128 v = ((__int128)limbs[2 * stride + i] << (2 * bits)) +
@@ -183,7 +186,13 @@ __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stri
   const unsigned __int128 u = (unsigned __int128)(neg ? -v : v);
   const double mag = __ull2double_rn((unsigned long long)(u >> 64)) * 0x1p64 +
                      __ull2double_rn((unsigned long long)u);
-  grids[i] = (neg ? -mag : mag) * aux[2];
+  if (wins != nullptr) {
+    const int64_t c = i % grid_total;
+    int l = 0;
+    while (l + 1 < P && wins[l + 1].grid_off <= c) ++l;   // windows are laid out in order
+    inv_boost = ldexp(1.0, -(dmax - wins[l].d) * peak_exp);
+  }
+  grids[i] = ((neg ? -mag : mag) * aux[2]) * inv_boost;
 }
 
 void ensure_aux_streams(afs_plan* p) {
@@ -318,7 +327,8 @@ void spread_all(afs_plan* p, const double* alpha, int64_t lda, int R, cudaStream
   if (timed) AFS_CUDA(cudaEventRecord(p->wev_spread[p->P], s));
   if (det) {
     k_det_finalize<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
-        p->det_limbs, p->grid_total * p->max_rhs, cells, p->det_aux, p->grids, p->det_bits);
+        p->det_limbs, p->grid_total * p->max_rhs, cells, p->det_aux, p->grids, p->det_bits, p->d_win,
+        p->P, p->grid_total, p->det_dmax, p->det_peak_exp, 1.0);
   }
   AFS_CUDA(cudaGetLastError());
 }
@@ -362,9 +372,9 @@ void det_window_finalize(afs_plan* p, const Window& w, int R, cudaStream_t s) {
   const int64_t stride = p->grid_total * p->max_rhs;
   for (int r = 0; r < R; ++r) {
     const int64_t off = r * p->grid_total + w.grid_off;
-    k_det_finalize<<<(unsigned)((w.cells + 255) / 256), 256, 0, s>>>(p->det_limbs + off, stride,
-                                                                     w.cells, p->det_aux,
-                                                                     p->grids + off, p->det_bits);
+    k_det_finalize<<<(unsigned)((w.cells + 255) / 256), 256, 0, s>>>(
+        p->det_limbs + off, stride, w.cells, p->det_aux, p->grids + off, p->det_bits, nullptr, 0,
+        p->grid_total, p->det_dmax, p->det_peak_exp, 1.0 / w.det_boost);
   }
   AFS_CUDA(cudaGetLastError());
 }
