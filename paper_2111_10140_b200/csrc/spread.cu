@@ -188,9 +188,14 @@ __global__ void k_det_finalize(const long long* __restrict__ limbs, int64_t stri
                      __ull2double_rn((unsigned long long)u);
   if (wins != nullptr) {
     const int64_t c = i % grid_total;
-    int l = 0;
-    while (l + 1 < P && wins[l + 1].grid_off <= c) ++l;   // windows are laid out in order
-    inv_boost = ldexp(1.0, -(dmax - wins[l].d) * peak_exp);
+    int lo = 0, hi = P - 1;   // windows are laid out in order of grid_off
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (wins[mid].grid_off <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    // 2^-k built from its exponent bits (k = (d_max - d) e < 1023)
+    inv_boost = __longlong_as_double((long long)(1023 - (dmax - wins[lo].d) * peak_exp) << 52);
   }
   grids[i] = ((neg ? -mag : mag) * aux[2]) * inv_boost;
 }
