@@ -1,4 +1,5 @@
-"""Ad-hoc GPU fuzz: random operators against the oracle (python tools/fuzz_many.py [count]).
+"""Ad-hoc GPU fuzz: random operators against the oracle (python tools/fuzz_many.py [count];
+FUZZ_SEED=n for other case sequences, FUZZ_ONLY=k replays one case).
 Run it also with AFS_CHEB=1 AFS_CHEB_SPREAD=1 (the switches are read once per process) to force
 the Chebyshev 2-D kernels on every 2-D m = 4 window; operators are built in deterministic mode
 at random (window pipeline for <= 8 windows in both modes)."""
@@ -11,7 +12,7 @@ def clustered(rng, N, d, k=3, std=0.01):
     centers = rng.uniform(-0.2, 0.2, size=(k, d))
     X = centers[rng.integers(0, k, size=N)] + std * rng.standard_normal((N, d))
     return np.clip(X, -0.25, np.nextafter(0.25, 0.0))
-rng = np.random.default_rng(777)
+rng = np.random.default_rng(int(os.environ.get("FUZZ_SEED", "777")))
 worst = 0; fails = 0
 count = int(sys.argv[1]) if len(sys.argv) > 1 else 120
 for k in range(count):
