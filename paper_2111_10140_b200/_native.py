@@ -11,7 +11,7 @@ import ctypes
 import os
 import threading
 
-from .errors import DeviceError, NumericalError, ShapeError, ValidationError
+from .errors import STATUS_EXCEPTIONS, DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libanovafs.so")
 # tuning hook: AFS_LIB selects an in-tree variant build (tools/build_variant.sh)
@@ -140,12 +140,7 @@ def check(status: int):
     if status == AFS_OK:
         return
     msg = (_lib.afs_last_error() or b"").decode("utf-8", "replace") if _lib else ""
-    if status == AFS_ERR_SHAPE:
-        raise ShapeError(msg)
-    if status == AFS_ERR_VALIDATION:
-        raise ValidationError(msg)
-    if status == AFS_ERR_NUMERICAL:
-        raise NumericalError(msg)
-    if status == AFS_ERR_NOMEM:
-        raise MemoryError(msg)
+    exc = STATUS_EXCEPTIONS.get(status)
+    if exc is not None:
+        raise exc(msg)
     raise DeviceError(msg or f"anovafs status {status}")
