@@ -81,6 +81,9 @@ __global__ void __launch_bounds__(256) k_gather_1d_fused(const double* __restric
 }
 
 // ---- per-cell Chebyshev tables (m = 4, compile-time KB table) ------------------------------
+#ifndef AFS_G1D_THREADS
+#define AFS_G1D_THREADS 512    // one block per SM (the tables take most of its shared memory); 1024 measured slower
+#endif
 constexpr int kMax1dSub = 32;       // windows per launch
 constexpr int kMaxCells1d = 96;     // occupied cells per window the tables may cover
 constexpr int kRow1d = 12;          // Chebyshev terms per half-cell (kb_cheb.inc)
@@ -109,7 +112,7 @@ __device__ __forceinline__ int mod_cell(int v, int n) {
 // Ghat[c][h][k] = sum_o Cc[h ? 7 - o : o][k] g[c - 3 + o]: the half-cell series of tc2d.cuh in
 // one dimension (h: the reflection class f > 1/2, variable u = 4 ((h ? 1 - f : f) - 1/4))
 template <int TAB>
-__global__ void __launch_bounds__(512) k_gather_1d_sub(const double* __restrict__ Z, int64_t N, int dtot,
+__global__ void __launch_bounds__(AFS_G1D_THREADS) k_gather_1d_sub(const double* __restrict__ Z, int64_t N, int dtot,
                                                        int n, const Gather1dSubBatch B,
                                                        const double* __restrict__ grid,
                                                        double* __restrict__ out) {
@@ -264,9 +267,9 @@ static void gather_1d_sub(afs_plan* p, const std::vector<int>& ws, double* out, 
     const size_t smem = sizeof(double) * (8 * kRow1d + B.gs_total + B.tab_total);
     auto launch = [&](auto k) {
       AFS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const int64_t blocks = std::min<int64_t>((p->Nt + 511) / 512, 148);
+      const int64_t blocks = std::min<int64_t>((p->Nt + AFS_G1D_THREADS - 1) / AFS_G1D_THREADS, 148);
       for (int r = 0; r < R; ++r)
-        k<<<(unsigned)std::max<int64_t>(1, blocks), 512, smem, s>>>(Z, p->Nt, p->dtot, p->n, B,
+        k<<<(unsigned)std::max<int64_t>(1, blocks), AFS_G1D_THREADS, smem, s>>>(Z, p->Nt, p->dtot, p->n, B,
                                                                     p->grids + r * p->grid_total,
                                                                     out + r * ldo);
     };
