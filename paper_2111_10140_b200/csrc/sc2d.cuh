@@ -31,6 +31,11 @@
 #ifndef AFS_SC_MINB_GATHER
 #define AFS_SC_MINB_GATHER 4
 #endif
+// 1: the spread's B fragments T_l(t1) are evaluated by the fragment lanes (monomial form)
+// instead of being transposed through shared memory
+#ifndef AFS_SC_BLANE
+#define AFS_SC_BLANE 1
+#endif
 #ifndef AFS_SC_MINB_SPREAD
 #define AFS_SC_MINB_SPREAD 4
 #endif
@@ -254,13 +259,39 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
     double* __restrict__ grid, int gpw) {
   constexpr int U = 4;
   __shared__ __align__(16) double chx[4][8][kScStride];   // alpha T_k(t0) [k][node]
+#if AFS_SC_BLANE
+  __shared__ __align__(16) double cty[4][32];               // t1 [node]: T_l(t1) is evaluated by the fragment lanes
+#else
   __shared__ __align__(16) double chy[4][8][kScStride];   // T_l(t1) [l][node]
+#endif
   __shared__ __align__(16) double csub[kScSub * 64];
   sc_load_coefs<TAB>(csub);
   const int lane = threadIdx.x & 31, slot = lane >> 2, q = lane & 3;
   const int wib = threadIdx.x >> 5;
   double(*CX)[kScStride] = chx[wib];
+#if AFS_SC_BLANE
+  double* CT = cty[wib];
+  // T_slot(t) = (slot odd ? t : 1) * P(t^2) with the lane's monomial coefficients: the B fragment
+  // T_l(t1[node]) is evaluated where it is used (5 fp64 operations per value) instead of being
+  // transposed through shared memory; the high orders' cancellation (T_7: 239 eps) is
+  // weighted by Chebyshev coefficients below 1e-14 of the window's peak
+  double pc[4];
+  {
+    constexpr double P[8][4] = {{1, 0, 0, 0},    {1, 0, 0, 0},       {-1, 2, 0, 0},      {-3, 4, 0, 0},
+                                {1, -8, 8, 0},   {5, -20, 16, 0},    {-1, 18, -48, 32},  {-7, 56, -112, 64}};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double c = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k == slot) c = P[k][j];
+      pc[j] = c;
+    }
+  }
+  const bool odd = slot & 1;
+#else
   double(*CY)[kScStride] = chy[wib];
+#endif
   const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int g0 = warp * gpw;
   if (g0 >= sv.ngroups) return;   // warp-uniform (after the block-wide table load)
@@ -347,8 +378,19 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
         const double u2 = 2.0 * t0, v2 = 2.0 * t1;
         double tx0 = al, tx1 = al * t0, ty0 = 1.0, ty1 = t1;   // alpha rides the x recurrence
         CX[0][lane] = tx0;
-        CY[0][lane] = 1.0;
         CX[1][lane] = tx1;
+#if AFS_SC_BLANE
+        CT[lane] = t1;
+        (void)v2, (void)ty0, (void)ty1;
+#pragma unroll
+        for (int k = 2; k < 8; ++k) {
+          const double tx2 = fma(u2, tx1, -tx0);
+          CX[k][lane] = tx2;
+          tx0 = tx1;
+          tx1 = tx2;
+        }
+#else
+        CY[0][lane] = 1.0;
         CY[1][lane] = t1;
 #pragma unroll
         for (int k = 2; k < 8; ++k) {
@@ -360,6 +402,7 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
           ty0 = ty1;
           ty1 = ty2;
         }
+#endif
       }
       int32_t hd[U];
 #pragma unroll
@@ -375,7 +418,13 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
           const int nd = u * 8 + q + 4 * s2;
+#if AFS_SC_BLANE
+          const double tv = CT[nd], z = tv * tv;
+          const double pz = fma(fma(fma(pc[3], z, pc[2]), z, pc[1]), z, pc[0]);
+          dmma884(acc[u], CX[slot][nd], odd ? pz * tv : pz);
+#else
           dmma884(acc[u], CX[slot][nd], CY[slot][nd]);
+#endif
         }
       }
     }
