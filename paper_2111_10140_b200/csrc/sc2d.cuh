@@ -36,6 +36,10 @@
 #ifndef AFS_SC_BLANE
 #define AFS_SC_BLANE 1
 #endif
+// 1: also the A fragments alpha T_k(t0) (no transposed tables at all: t0, t1, alpha broadcast)
+#ifndef AFS_SC_ALANE
+#define AFS_SC_ALANE 0
+#endif
 #ifndef AFS_SC_MINB_SPREAD
 #define AFS_SC_MINB_SPREAD 4
 #endif
@@ -260,6 +264,9 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
   constexpr int U = 4;
   __shared__ __align__(16) double chx[4][8][kScStride];   // alpha T_k(t0) [k][node]
 #if AFS_SC_BLANE
+#if AFS_SC_ALANE
+  __shared__ __align__(16) double ctx[4][32], cta[4][32];   // t0, alpha [node]
+#endif
   __shared__ __align__(16) double cty[4][32];               // t1 [node]: T_l(t1) is evaluated by the fragment lanes
 #else
   __shared__ __align__(16) double chy[4][8][kScStride];   // T_l(t1) [l][node]
@@ -271,6 +278,10 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
   double(*CX)[kScStride] = chx[wib];
 #if AFS_SC_BLANE
   double* CT = cty[wib];
+#if AFS_SC_ALANE
+  double* CT0 = ctx[wib];
+  double* CA = cta[wib];
+#endif
   // T_slot(t) = (slot odd ? t : 1) * P(t^2) with the lane's monomial coefficients: the B fragment
   // T_l(t1[node]) is evaluated where it is used (5 fp64 operations per value) instead of being
   // transposed through shared memory; the high orders' cancellation (T_7: 239 eps) is
@@ -377,9 +388,14 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
       {   // this lane's node: alpha T_k(t0) and T_l(t1), k, l < 8, into the transposed tables
         const double u2 = 2.0 * t0, v2 = 2.0 * t1;
         double tx0 = al, tx1 = al * t0, ty0 = 1.0, ty1 = t1;   // alpha rides the x recurrence
+#if AFS_SC_BLANE && AFS_SC_ALANE
+        CT[lane] = t1;
+        CT0[lane] = t0;
+        CA[lane] = al;
+        (void)u2, (void)v2, (void)tx0, (void)tx1, (void)ty0, (void)ty1;
+#elif AFS_SC_BLANE
         CX[0][lane] = tx0;
         CX[1][lane] = tx1;
-#if AFS_SC_BLANE
         CT[lane] = t1;
         (void)v2, (void)ty0, (void)ty1;
 #pragma unroll
@@ -390,6 +406,8 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
           tx1 = tx2;
         }
 #else
+        CX[0][lane] = tx0;
+        CX[1][lane] = tx1;
         CY[0][lane] = 1.0;
         CY[1][lane] = t1;
 #pragma unroll
@@ -418,7 +436,13 @@ __global__ void __launch_bounds__(128, AFS_SC_MINB_SPREAD) k_spread_sc(
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
           const int nd = u * 8 + q + 4 * s2;
-#if AFS_SC_BLANE
+#if AFS_SC_BLANE && AFS_SC_ALANE
+          const double tv = CT[nd], z = tv * tv;
+          const double pz = fma(fma(fma(pc[3], z, pc[2]), z, pc[1]), z, pc[0]);
+          const double tu = CT0[nd], zu = tu * tu;
+          const double pu = fma(fma(fma(pc[3], zu, pc[2]), zu, pc[1]), zu, pc[0]);
+          dmma884(acc[u], (odd ? pu * tu : pu) * CA[nd], odd ? pz * tv : pz);
+#elif AFS_SC_BLANE
           const double tv = CT[nd], z = tv * tv;
           const double pz = fma(fma(fma(pc[3], z, pc[2]), z, pc[1]), z, pc[0]);
           dmma884(acc[u], CX[slot][nd], odd ? pz * tv : pz);
