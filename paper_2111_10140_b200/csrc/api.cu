@@ -469,6 +469,18 @@ static void create_plan(const afs_plan_desc* d, afs_plan** out) {
           };
           p->src_side[l] = new SortedSide();
           build(p->src, p->Ns, p->src_side[l], true);
+          // 2-D windows between the two density rules (C5's pairs: ~34 nodes per sub-cell): the sub-cell
+          // gather already wins there (0.029-0.031 vs 0.033 ms), the sub-cell spread does not, so the
+          // gather gets its own sub-cell layout of the sources (C5 0.818 -> 0.786 ms per matvec;
+          // 20 N bytes more per window; AFS_DUAL2=0 keeps one layout)
+          if (scw && !p->has_targets && !p->src_side[l]->sc) {
+            const char* e = getenv("AFS_DUAL2");
+            if (!(e && e[0] == '0')) {
+              SortedSide* gs = new SortedSide();
+              if (build_sorted_side_sc(p, w, p->src, p->Ns, gs, sc, 0.2, 24.0)) p->tgt_side[l] = gs;
+              else delete gs;
+            }
+          }
           if (dual3 && !p->has_targets) {
             SortedSide* gs = new SortedSide();
             if (build_sorted_side_tc3(p, w, p->src, p->Ns, gs, sc, 0.15, false)) p->tgt_side[l] = gs;

@@ -611,7 +611,7 @@ bool sc_eligible(int d, int m, int tab, int n, int64_t N) {
 }
 
 bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
-                          BuildScratch& sc, double max_padding) {
+                          BuildScratch& sc, double max_padding, double min_nodes) {
   const int n = p->n;
   const cudaStream_t s = 0;
   int bits = 1;
@@ -663,7 +663,7 @@ bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t
     // flushes 64 cells per sub-cell and warp: at C5's ~34 nodes per sub-cell it takes 0.065-0.08
     // ms against 0.04 ms for the half-cell kernels; at C3's ~98 it is 25% faster)
     const bool dense = (double)(total - N) <= max_padding * (double)N &&
-                       (max_padding > 1e29 || (double)N >= 64.0 * (double)nruns);
+                       (max_padding > 1e29 || (double)N >= min_nodes * (double)nruns);
     if (getenv("AFS_VERBOSE"))
       fprintf(stderr, "[afs] sub-cell layout: N=%lld sub-cells=%d (%.1f nodes each) padding +%.1f%% -> %s\n",
               (long long)N, nruns, (double)N / (double)nruns, 100.0 * (double)(total - N) / (double)N,

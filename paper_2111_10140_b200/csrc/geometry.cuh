@@ -89,7 +89,7 @@ bool build_sorted_side_tc3(afs_plan* p, const Window& w, const double* X, int64_
 // groups of 8 would add more than max_padding * N nodes
 bool sc_eligible(int d, int m, int tab, int n, int64_t N);
 bool build_sorted_side_sc(afs_plan* p, const Window& w, const double* X, int64_t N, SortedSide* out,
-                          BuildScratch& sc, double max_padding);
+                          BuildScratch& sc, double max_padding, double min_nodes = 64.0);
 constexpr int kScSub = 16;   // sub-intervals per cell and dimension (kb_sub.inc)
 __host__ __device__ __forceinline__ int32_t sc_header(int u0, int u1, int s0, int s1) {
   return (int32_t)((uint32_t)u0 | ((uint32_t)u1 << 12) | ((uint32_t)s0 << 24) | ((uint32_t)s1 << 28));
